@@ -1,0 +1,197 @@
+/*
+ * bdlora.h -- C ABI of the B200-native BD-LoRA tensor-parallel multi-adapter LoRA layer.
+ *
+ * Paper: "Block-diagonal LoRA" (BD-LoRA), arXiv 2510.23346 (PAPER.md, cited as P:<line>).
+ *
+ * The layer, per token t with adapter a(t) from a resident pool:
+ *
+ *     y_t = x_t W + s_a * (x_t A_a) B_a
+ *
+ * sharded Megatron-style over N = tp_size devices:
+ *   column-parallel (QKV, gate|up):  W, A column-sharded, B BLOCK-DIAGONAL   (Alg. 2)
+ *   row-parallel    (O, down):       W row-sharded, A BLOCK-DIAGONAL, B row-sharded, one all-reduce
+ *                                    of the base+LoRA partial                 (Alg. 1)
+ * so BD-LoRA adds ZERO collectives.  The S-LoRA sharding is provided as the comparison
+ * path: +1 all-gather per column layer, +1 all-reduce per row layer.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns a bdlora_status; on failure bdlora_last_error() (thread-local) names
+ *     the offending argument / shape / value.  No C++ exception crosses this boundary.
+ *   - Tensors are plain pointers.  "device" pointers are CUDA device memory of the pool's device;
+ *     bf16 = IEEE bfloat16 (uint16 storage), row-major, densely packed unless an ld is given.
+ *   - Ownership: the caller owns X, W, Y, ids and the workspace; the library never frees them.
+ *     The pool owns adapter memory.  The comm owns its ncclComm_t.
+ *   - Streams: all device work is enqueued on `stream` (a cudaStream_t passed as void*, 0 = legacy
+ *     default).  Forward calls do no allocation, no host synchronisation and no device-side
+ *     validation, so they are CUDA-graph capturable.  Validation is on host-side shapes only;
+ *     asynchronous CUDA faults surface on a later call as BDLORA_E_CUDA.
+ *   - ids contract: ids[t] in [-1, capacity) and referring to a LOADED slot; -1 = no adapter
+ *     (LoRA term exactly 0, reading R8).  Not checked on device.
+ *   - A pool is not thread-safe; distinct pools / devices are independent.
+ *   - Numerics (reading R7): bf16 inputs, fp32 accumulation, the LoRA intermediate
+ *     v = s * x A is kept in fp32 (also for the S-LoRA collective payloads), the base and LoRA
+ *     terms are summed in fp32 and rounded to bf16 ONCE (RNE).  Row partials are rounded to bf16
+ *     before the bf16 all-reduce.
+ *   - N == 1: BD == S-LoRA == plain LoRA, no NCCL call is made.  T == 0: no-op (BDLORA_OK).
+ *   - Layout deviation (documented in DESIGN.md): the paper writes W in R^{d_in x d_out}; the
+ *     ABI takes W^T, i.e. [d_out_loc, d_in_loc] row-major ("nn.Linear.weight" / K-major), which makes
+ *     both tensor-core operands K-major.  Adapter factors are given in the paper's orientation.
+ *
+ * Build: sm_100a only (-gencode arch=compute_100a,code=sm_100a); other devices -> BDLORA_E_ARCH.
+ */
+#ifndef BDLORA_H_
+#define BDLORA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BDLORA_ABI_VERSION 1
+#define BDLORA_UNIQUE_ID_BYTES 128
+#define BDLORA_MAX_SLICES 3
+
+typedef struct bdlora_pool bdlora_pool; /* opaque: one per (device, projection, sharding mode)  */
+typedef struct bdlora_comm bdlora_comm; /* opaque: wraps an ncclComm_t owned by the library      */
+typedef void* bdlora_stream_t;          /* cudaStream_t                                          */
+
+typedef enum {
+  BDLORA_OK = 0,
+  BDLORA_E_ARG = 1,          /* null pointer, negative size, shape mismatch, bad enum          */
+  BDLORA_E_DIVISIBILITY = 2, /* d_in / d_out / rank not divisible by tp_size          */
+  BDLORA_E_CAPACITY = 3,     /* slot out of range, rank > max_rank, arena full, T too large     */
+  BDLORA_E_NOT_LOADED = 4,   /* slot not loaded (unload / host-side checks)                     */
+  BDLORA_E_MODE = 5,         /* BD pool passed to slora_* or vice versa, row pool to column fn  */
+  BDLORA_E_CUDA = 6,         /* CUDA runtime error (message has cudaGetErrorString)             */
+  BDLORA_E_NCCL = 7,         /* NCCL error                                                      */
+  BDLORA_E_ARCH = 8          /* device is not sm_100 (compute capability 10.0)                  */
+} bdlora_status;
+
+enum { BDLORA_COLUMN = 0, BDLORA_ROW = 1 };
+enum { BDLORA_SHARD_BD = 0, BDLORA_SHARD_SLORA = 1 };
+
+typedef struct {
+  int32_t parallel;   /* BDLORA_COLUMN | BDLORA_ROW                                              */
+  int32_t sharding;   /* BDLORA_SHARD_BD | BDLORA_SHARD_SLORA                                    */
+  int32_t tp_size;    /* N >= 1                                                                  */
+  int32_t tp_rank;    /* i in [0, N): block i lives on device i (reading R2)          */
+  int32_t d_in;       /* FULL input dim                                                          */
+  int32_t n_slices;   /* J: 1; 2 = gate|up; 3 = q|k|v (each slice has its own A, B; reading R4).
+                         ROW requires 1.                                                         */
+  int32_t d_out[BDLORA_MAX_SLICES]; /* FULL output dim per slice                                 */
+  int32_t capacity;   /* resident adapter slots (ids index these)                                */
+  int32_t max_rank;   /* full-rank bound r_max; BD requires tp_size | every loaded rank          */
+  int64_t arena_bytes;/* 0 = capacity x max_rank sizing; else a ragged first-fit arena of this size*/
+} bdlora_pool_desc;
+
+/* ---------------------------------------------------------------- library / device ---------- */
+int bdlora_abi_version(void);
+const char* bdlora_last_error(void); /* thread-local, never NULL; "" when no error            */
+/* BDLORA_OK iff `cuda_device` is sm_100 (CC 10.0) and the library's kernels can run on it.     */
+int bdlora_device_check(int cuda_device);
+
+/* ---------------------------------------------------------------- communicator (NCCL) ------- */
+/* NCCL 2.28 over NVLink/NVSwitch.  Bootstrap: rank 0 calls bdlora_comm_unique_id, the caller
+   broadcasts the 128 bytes (e.g. torch.distributed.broadcast), every rank calls bdlora_comm_init. */
+int bdlora_comm_unique_id(uint8_t id[BDLORA_UNIQUE_ID_BYTES]);
+int bdlora_comm_init(const uint8_t id[BDLORA_UNIQUE_ID_BYTES], int nranks, int rank, int cuda_device,
+                     bdlora_comm** out);
+int bdlora_comm_destroy(bdlora_comm* comm);
+/* Collective call log since init (SPEC S:148 per-tag counters):
+   counts[0] base all-reduce calls, [1] LoRA all-gather calls, [2] LoRA all-reduce calls,
+   [3] base all-reduce bytes, [4] LoRA all-gather bytes (per rank, sent), [5] LoRA all-reduce bytes.
+   BD-LoRA paths never touch counts[1], [2], [4], [5] (Fig. 3 caption).               */
+int bdlora_comm_stats(const bdlora_comm* comm, int64_t counts[6]);
+
+/* ---------------------------------------------------------------- adapter pool -------------- */
+int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_pool** out);
+int bdlora_destroy_pool(bdlora_pool* pool);
+
+/* Copies the FULL (unsharded) factors of one adapter and keeps only device tp_rank's shard
+   ("modified the slicing code"), stored compactly -- no zero of a block-diagonal
+   factor is stored or touched.  A[j], B[j] are bf16, paper orientation, row-major:
+     COLUMN + BD   : A[j] d_in x r ;  B[j] compact (r/N) x d_out[j], the N diagonal blocks
+                     (r/N) x (d_out[j]/N) side by side
+     ROW    + BD   : A[0] compact d_in x (r/N), the N diagonal blocks (d_in/N) x (r/N) stacked
+                      ;  B[0] r x d_out
+     *      + SLORA: dense A[j] d_in x r ;  B[j] r x d_out[j]
+   rank r: 1 <= r <= max_rank, BD needs N | r (else BDLORA_E_DIVISIBILITY).  scale = s_a applied to
+   the fp32 shrink output (e.g. alpha*sqrt(N)/sqrt(r) for BD; reading R1).  src_is_device:
+   0 = host pointers (copied synchronously w.r.t. `stream`; sources may be freed on return),
+   1 = device pointers (caller may free after `stream` completes).  Reloading a loaded slot
+   replaces it.                                                                                  */
+int bdlora_load_adapter(bdlora_pool* pool, int32_t slot, int32_t rank, float scale,
+                        const void* const* A, const void* const* B, int32_t src_is_device,
+                        bdlora_stream_t stream);
+int bdlora_unload_adapter(bdlora_pool* pool, int32_t slot);
+/* Resident adapter bytes (compact shards) and arena capacity in bytes.                          */
+int bdlora_pool_bytes(const bdlora_pool* pool, int64_t* resident, int64_t* arena);
+/* Local geometry: K_loc (input dim of X on this device) and M_loc (output columns on this
+   device: sum_j d_out[j]/N for COLUMN, d_out[0] for ROW).                                        */
+int bdlora_pool_geometry(const bdlora_pool* pool, int32_t* k_loc, int32_t* m_loc);
+
+/* Workspace bytes needed by any forward of this pool for T tokens (device memory, caller-owned,
+   256-byte aligned base, reusable across calls on the same stream, contents undefined on entry). */
+int bdlora_workspace_bytes(const bdlora_pool* pool, int64_t T, size_t* bytes);
+
+/* ---------------------------------------------------------------- routing metadata (a2) ----- */
+/* Segments = maximal runs of equal consecutive ids in token order (reading R10): writes
+   seg_start/seg_len/seg_id[0..n) and *n_seg_dev = n (all device int32 arrays of >= T entries).
+   Bit-exact with the oracle's RLE.  Used by the prefill (SGMV) path; exposed for testing.       */
+int bdlora_build_segments(const int32_t* ids, int64_t T, int32_t* seg_start, int32_t* seg_len,
+                          int32_t* seg_id, int32_t* n_seg_dev, bdlora_stream_t stream);
+
+/* ---------------------------------------------------------------- BD-LoRA forward ----------- */
+/* Column layer, Alg. 2 lines 3-6 on device tp_rank -- NO communication:
+     Y_i = X W_i + s_a (X A_i[a]) B_i[a]
+   X  [T, d_in] bf16 (replicated input);  W = W_i^T as [M_loc, d_in] bf16 with the slices stacked
+   (q_i | k_i | v_i rows);  ids [T] int32 device;  Y [T, M_loc] bf16 = [q_i | k_i | v_i] columns.
+   Pool: COLUMN + BD.                                                                            */
+int bdlora_column_forward(bdlora_pool* pool, const void* X, int64_t T, const void* W, const int32_t* ids,
+                          void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+
+/* Row layer partial, Alg. 1 lines 9-12 on device tp_rank, WITHOUT the all-reduce:
+     P_i = X_i W_i + s_a (X_i A_i[a]) B_i[a]       (A_i = diagonal block, B_i = row shard)
+   X [T, d_in/N] bf16;  W = W_i^T as [d_out, d_in/N] bf16;  P [T, d_out] bf16.  Pool: ROW + BD.   */
+int bdlora_row_partial(bdlora_pool* pool, const void* X, int64_t T, const void* W, const int32_t* ids,
+                       void* P, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+
+/* Row layer, Alg. 1 lines 9-15: Y = AllReduce_i(P_i), the base model's own all-reduce -- the only
+   collective of BD-LoRA.  Y [T, d_out] bf16, replicated; in-place NCCL bf16 sum.
+   comm may be NULL iff tp_size == 1.                                                             */
+int bdlora_row_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
+                       const int32_t* ids, void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+
+/* ---------------------------------------------------------------- S-LoRA comparison --------- */
+/* Column: v_i = s X A[:, chunk i] -> ncclAllGather -> v [T, r] -> Y_i = X W_i + v B[:, cols i].
+   Same tensors as bdlora_column_forward; pool COLUMN + SLORA.  +1 all-gather (merged over the
+   J slices, P:340-341 footnote).                                                                 */
+int slora_column_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
+                         const int32_t* ids, void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+/* Row (reading R12): v_i = s X_i A[rows i, :] -> ncclAllReduce -> v [T, r] ->
+   P_i = X_i W_i, P_i[:, cols i] += v B[:, cols i] (the fused all-gather, zero extra traffic)
+   -> base ncclAllReduce.  Pool ROW + SLORA.  +1 all-reduce.                                      */
+int slora_row_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
+                      const int32_t* ids, void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+
+/* ---------------------------------------------------------------- phases -------------------- */
+/* The two device-local halves of every path, for callers that run the collective themselves
+   (e.g. tests emulating N ranks on one GPU).  v is fp32 with layout [C][T][J][R_c]:
+     R_c = max_rank/N (BD, S-LoRA column) or max_rank (S-LoRA row);  C = 1 except S-LoRA column
+     after the all-gather, C = N (rank-major, chunk c = device c's shrink).
+   bdlora_lora_shrink writes this device's [T][J][R_c] (C = 1):  v = s_a * X A_i[a]  (matmul_3/5).
+   bdlora_base_expand computes Y = X W_i + expand(v) (matmul_1/2 + matmul_4/6 + add_1/2) reading v
+   in the pool's post-collective layout (S-LoRA column: C = N).                                  */
+int bdlora_lora_shrink(bdlora_pool* pool, const void* X, int64_t T, const int32_t* ids, float* v,
+                       void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+int bdlora_base_expand(bdlora_pool* pool, const void* X, int64_t T, const void* W, const int32_t* ids,
+                       const float* v, void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+/* Elements of one device's v (= T * J * R_c) for this pool.                                      */
+int bdlora_v_elems(const bdlora_pool* pool, int64_t T, int64_t* elems);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDLORA_H_ */

@@ -1,0 +1,98 @@
+// common.cuh -- device-side data structures shared by all bdlora kernels (sm_100a).
+//
+// Pool layout in HBM: one bf16 arena per pool; each loaded slot keeps
+// only this device's shard of its factors, stored compactly (no zero of a block-diagonal factor is
+// stored):
+//   A_j : [rs, K]   rank-outermost, K contiguous  (the shrink streams whole 128-bit rows)
+//   B_j : [re, ldb_j] row-major, output columns contiguous (the expand epilogue reads a row of B
+//         across consecutive output columns -> coalesced)
+// and one 64-byte SlotEntry in a device table indexed by the adapter id.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bdl {
+
+constexpr int kMaxSlices = 3;
+
+struct SlotEntry {
+  long long offA[kMaxSlices];  // element offsets into the arena
+  long long offB[kMaxSlices];
+  int rs;       // shrink rank: rows of A_j on this device (BD: r/N, S-LoRA col: r/N, S-LoRA row: r)
+  int re;       // expand rank: rows of B_j on this device (BD: r/N, S-LoRA: r)
+  float scale;  // s_a
+  int loaded;
+};
+static_assert(sizeof(SlotEntry) == 64, "SlotEntry must stay 64 bytes");
+
+// Local geometry of one projection on one device.
+struct Geom {
+  int K;                  // input dim of X on this device
+  int M;                  // output columns on this device (rows of W^T)
+  int J;                  // slices
+  int col0[kMaxSlices + 1];  // local column start of slice j; col0[J] = M
+  int e_lo[kMaxSlices];   // expand window of slice j, absolute local columns [e_lo, e_hi)
+  int e_hi[kMaxSlices];
+  int Rc;                 // per-chunk rank capacity of v
+  int C;                  // chunks of v read by the expand (S-LoRA column after all-gather: N)
+};
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float f[8]) {
+  f[0] = __uint_as_float(u.x << 16);
+  f[1] = __uint_as_float(u.x & 0xffff0000u);
+  f[2] = __uint_as_float(u.y << 16);
+  f[3] = __uint_as_float(u.y & 0xffff0000u);
+  f[4] = __uint_as_float(u.z << 16);
+  f[5] = __uint_as_float(u.z & 0xffff0000u);
+  f[6] = __uint_as_float(u.w << 16);
+  f[7] = __uint_as_float(u.w & 0xffff0000u);
+}
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+
+// Streaming 128-bit load that does not allocate in L1 (weights are read exactly once).
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint4 ld_cached_u4(const void* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// LoRA expand term for output column n of token t:  sum_c sum_k v[c][t][j][k] * B_j[c*re/C + k][n - e_lo_j]
+// (matmul_4 / matmul_6).  Returns 0 outside the expand window or for id -1.
+__device__ __forceinline__ float lora_expand_term(int t, int n, int a, const SlotEntry* __restrict__ tab,
+                                                  const __nv_bfloat16* __restrict__ arena, const Geom& g,
+                                                  const float* __restrict__ v, int T) {
+  if (a < 0) return 0.f;
+  int j = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxSlices; ++q)
+    if (q < g.J && n >= g.col0[q]) j = q;
+  if (n < g.e_lo[j] || n >= g.e_hi[j]) return 0.f;
+  const SlotEntry& e = tab[a];
+  const int ldb = g.e_hi[j] - g.e_lo[j];
+  const int col = n - g.e_lo[j];
+  const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + e.offB[j]);
+  const int rc = e.re / g.C;
+  float s = 0.f;
+  for (int c = 0; c < g.C; ++c) {
+    const float* vv = v + ((size_t)(c * T + t) * g.J + j) * g.Rc;
+    const uint16_t* Bc = B + (size_t)(c * rc) * ldb + col;
+    for (int k = 0; k < rc; ++k) s = fmaf(vv[k], bf16_bits_to_f32(__ldg(Bc + (size_t)k * ldb)), s);
+  }
+  return s;
+}
+
+}  // namespace bdl

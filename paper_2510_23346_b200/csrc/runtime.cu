@@ -1,0 +1,793 @@
+// runtime.cu -- the C-ABI of libbdlora.so (include/bdlora.h): pool arena + tables, adapter loader /
+// slicer, host-side validation, workspace sizing, NCCL communicator, launch sequencing of the
+// BD-LoRA and S-LoRA paths.  sm_100a only.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/bdlora.h"
+#include "common.cuh"
+#include "kernels_core.cuh"
+#include "kernels_umma.cuh"
+
+using bdl::Geom;
+using bdl::SlotEntry;
+
+// ============================================================================ errors
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU_TRY(expr)                                                                            \
+  do {                                                                                          \
+    cudaError_t _e = (expr);                                                                    \
+    if (_e != cudaSuccess) return fail(BDLORA_E_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                                       __FILE__, __LINE__);                                     \
+  } while (0)
+
+#define NC_TRY(expr)                                                                            \
+  do {                                                                                          \
+    ncclResult_t _r = (expr);                                                                   \
+    if (_r != ncclSuccess) return fail(BDLORA_E_NCCL, "%s: %s", #expr, ncclGetErrorString(_r)); \
+  } while (0)
+
+#define ST_TRY(expr)            \
+  do {                          \
+    int _s = (expr);            \
+    if (_s != BDLORA_OK) return _s; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = (cudaSetDevice(dev) == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+// ============================================================================ objects
+struct bdlora_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0, dev = 0;
+  int64_t counts[6] = {0, 0, 0, 0, 0, 0};
+};
+
+struct bdlora_pool {
+  bdlora_pool_desc d;
+  int dev = 0;
+  Geom g;               // local geometry (C = chunks read by the expand)
+  int rs_max = 0;       // shrink rank capacity per slot
+  int re_max = 0;       // expand rank capacity per slot
+  int ldb[bdl::kMaxSlices] = {0, 0, 0};
+  uint16_t* arena = nullptr;
+  int64_t arena_elems = 0;
+  SlotEntry* d_tab = nullptr;
+  std::vector<SlotEntry> h_tab;
+  std::vector<int64_t> slot_elems;       // elems held by each slot (0 = empty)
+  std::map<int64_t, int64_t> free_list;  // ragged arena: offset -> length (elements)
+  bool ragged = false;
+  int64_t resident_elems = 0;
+  int num_sms = 148;
+};
+
+namespace {
+
+int64_t slot_elems_for_rank(const bdlora_pool* p, int r) {
+  const auto& d = p->d;
+  const int N = d.tp_size;
+  int rs, re;
+  if (d.sharding == BDLORA_SHARD_BD) {
+    rs = r / N;
+    re = r / N;
+  } else if (d.parallel == BDLORA_COLUMN) {
+    rs = r / N;
+    re = r;
+  } else {
+    rs = r;
+    re = r;
+  }
+  int64_t e = 0;
+  for (int j = 0; j < p->g.J; ++j) e += (int64_t)rs * p->g.K + (int64_t)re * p->ldb[j];
+  return e;
+}
+
+void ranks_for(const bdlora_pool* p, int r, int* rs, int* re) {
+  const auto& d = p->d;
+  const int N = d.tp_size;
+  if (d.sharding == BDLORA_SHARD_BD) {
+    *rs = r / N;
+    *re = r / N;
+  } else if (d.parallel == BDLORA_COLUMN) {
+    *rs = r / N;
+    *re = r;
+  } else {
+    *rs = r;
+    *re = r;
+  }
+}
+
+// Workspace layout (bytes, 256-aligned sections):
+//   [counters: int32 x kMaxTiles][v: C_w x T x J x Rc fp32][part: S*T x M fp32 (split-K partials)]
+constexpr int kMaxTiles = 8192;
+constexpr int kPartTokenSplits = 64;  // S x min(T, 8) <= 64 for the split-K GEMV
+
+struct WsLayout {
+  size_t off_counters, off_v, off_part, off_umma, total;
+};
+
+WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
+  WsLayout L;
+  size_t o = 0;
+  L.off_counters = o;
+  o = align_up(o + sizeof(int) * kMaxTiles, 256);
+  L.off_v = o;
+  const int Cw = (p->d.sharding == BDLORA_SHARD_SLORA && p->d.parallel == BDLORA_COLUMN) ? p->d.tp_size : 1;
+  o = align_up(o + sizeof(float) * (size_t)Cw * T * p->g.J * p->g.Rc, 256);
+  L.off_part = o;
+  o = align_up(o + sizeof(float) * (size_t)kPartTokenSplits * p->g.M, 256);
+  L.off_umma = o;
+  o = align_up(o + bdl::umma_workspace_bytes(p->g.M, (int)T), 256);
+  L.total = o;
+  return L;
+}
+
+int check_pool(const bdlora_pool* p) {
+  if (!p) return fail(BDLORA_E_ARG, "pool is NULL");
+  return BDLORA_OK;
+}
+
+int check_fwd_args(const bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, const void* Y,
+                   void* ws, size_t ws_bytes) {
+  ST_TRY(check_pool(p));
+  if (T < 0) return fail(BDLORA_E_ARG, "T = %lld < 0", (long long)T);
+  if (T > (1 << 20)) return fail(BDLORA_E_CAPACITY, "T = %lld exceeds 2^20 tokens", (long long)T);
+  if (T == 0) return BDLORA_OK;
+  if (!X || !W || !ids || !Y) return fail(BDLORA_E_ARG, "X/W/ids/Y must be non-NULL (X=%p W=%p ids=%p Y=%p)", X, W, ids, Y);
+  if (((uintptr_t)X | (uintptr_t)W) & 15) return fail(BDLORA_E_ARG, "X and W must be 16-byte aligned");
+  if (!ws) return fail(BDLORA_E_ARG, "workspace is NULL");
+  const size_t need = ws_layout(p, T).total;
+  if (ws_bytes < need)
+    return fail(BDLORA_E_ARG, "workspace too small: %zu < %zu bytes for T=%lld", ws_bytes, need, (long long)T);
+  if ((uintptr_t)ws & 255) return fail(BDLORA_E_ARG, "workspace must be 256-byte aligned");
+  return BDLORA_OK;
+}
+
+// ---------------------------------------------------------------------------- launches
+int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids, float* v, cudaStream_t st) {
+  if (T == 0) return BDLORA_OK;
+  const Geom& g = p->g;
+  dim3 grid(T, g.J, (p->rs_max + 7) / 8);
+  const size_t smem = sizeof(int) * (size_t)T;
+  bdl::shrink_kernel<4><<<grid, 256, smem, st>>>((const __nv_bfloat16*)X, T, ids, p->d_tab,
+                                                 (const __nv_bfloat16*)p->arena, g, v);
+  CU_TRY(cudaGetLastError());
+  return BDLORA_OK;
+}
+
+int launch_gemv(const bdlora_pool* p, const void* X, int T, const void* W, const int32_t* ids, const float* v,
+                void* Y, void* ws, cudaStream_t st) {
+  const Geom& g = p->g;
+  const WsLayout L = ws_layout(p, T);
+  char* base = (char*)ws;
+  int* counters = (int*)(base + L.off_counters);
+  float* part = (float*)(base + L.off_part);
+  constexpr int RW = 2, ROWS = 8 * RW;
+  const int ntiles = (g.M + ROWS - 1) / ROWS;
+  if (ntiles > kMaxTiles) return fail(BDLORA_E_CAPACITY, "M = %d too large for the GEMV path", g.M);
+  const int TT = T >= 8 ? 8 : (T >= 4 ? 4 : (T >= 2 ? 2 : 1));
+  // split-K so that the grid has >= ~4 CTAs (32 warps) per SM; partial buffer bounds S*T <= 64
+  int S = 1;
+  const int target = 4 * p->num_sms;
+  if (ntiles < target && T <= 8) {
+    S = (target + ntiles - 1) / ntiles;
+    S = std::min(S, std::max(1, g.K / 256));
+    S = std::min(S, kPartTokenSplits / std::max(T, 1));
+    S = std::max(S, 1);
+  }
+  int Kc = (g.K + S - 1) / S;
+  Kc = (Kc + 7) / 8 * 8;
+  S = (g.K + Kc - 1) / Kc;
+  dim3 grid(ntiles, S);
+#define GEMV_CASE(TTV)                                                                                      \
+  bdl::gemv_lora_kernel<TTV, RW><<<grid, 256, 0, st>>>((const __nv_bfloat16*)X, T, (const __nv_bfloat16*)W, ids, \
+                                                       p->d_tab, (const __nv_bfloat16*)p->arena, g, v,             \
+                                                       (__nv_bfloat16*)Y, part, counters, S, Kc)
+  switch (TT) {
+    case 1: GEMV_CASE(1); break;
+    case 2: GEMV_CASE(2); break;
+    case 4: GEMV_CASE(4); break;
+    default: GEMV_CASE(8); break;
+  }
+#undef GEMV_CASE
+  CU_TRY(cudaGetLastError());
+  return BDLORA_OK;
+}
+
+int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W, const int32_t* ids, const float* v,
+                       void* Y, void* ws, cudaStream_t st) {
+  if (T == 0) return BDLORA_OK;
+  if (bdl::umma_eligible(p->g, T)) {
+    const WsLayout L = ws_layout(p, T);
+    int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, T, (const __nv_bfloat16*)W, ids, p->d_tab,
+                              (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
+                              p->num_sms, st);
+    if (rc == 0) {
+      CU_TRY(cudaGetLastError());
+      return BDLORA_OK;
+    }
+    // rc != 0: shape not supported by the tensor-core kernel -> CUDA-core kernel (still on GPU)
+  }
+  return launch_gemv(p, X, T, W, ids, v, Y, ws, st);
+}
+
+float* ws_v(const bdlora_pool* p, void* ws, int64_t T) { return (float*)((char*)ws + ws_layout(p, T).off_v); }
+
+int require_mode(const bdlora_pool* p, int parallel, int sharding, const char* fn) {
+  if (p->d.parallel != parallel || p->d.sharding != sharding)
+    return fail(BDLORA_E_MODE, "%s: pool is %s+%s, expected %s+%s", fn, p->d.parallel == BDLORA_COLUMN ? "COLUMN" : "ROW",
+                p->d.sharding == BDLORA_SHARD_BD ? "BD" : "SLORA", parallel == BDLORA_COLUMN ? "COLUMN" : "ROW",
+                sharding == BDLORA_SHARD_BD ? "BD" : "SLORA");
+  return BDLORA_OK;
+}
+
+int require_comm(const bdlora_pool* p, const bdlora_comm* c, const char* fn) {
+  if (p->d.tp_size == 1) return BDLORA_OK;
+  if (!c) return fail(BDLORA_E_ARG, "%s: comm is NULL but tp_size = %d", fn, p->d.tp_size);
+  if (c->nranks != p->d.tp_size || c->rank != p->d.tp_rank)
+    return fail(BDLORA_E_ARG, "%s: comm (nranks=%d, rank=%d) does not match pool (tp_size=%d, tp_rank=%d)", fn,
+                c->nranks, c->rank, p->d.tp_size, p->d.tp_rank);
+  if (c->dev != p->dev) return fail(BDLORA_E_ARG, "%s: comm device %d != pool device %d", fn, c->dev, p->dev);
+  return BDLORA_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int bdlora_abi_version(void) { return BDLORA_ABI_VERSION; }
+
+const char* bdlora_last_error(void) { return g_err.c_str(); }
+
+int bdlora_device_check(int cuda_device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return fail(BDLORA_E_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  if (cuda_device < 0 || cuda_device >= n) return fail(BDLORA_E_ARG, "cuda_device %d out of range [0,%d)", cuda_device, n);
+  int maj = 0, min = 0;
+  CU_TRY(cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, cuda_device));
+  CU_TRY(cudaDeviceGetAttribute(&min, cudaDevAttrComputeCapabilityMinor, cuda_device));
+  if (maj != 10 || min != 0)
+    return fail(BDLORA_E_ARCH, "device %d is sm_%d%d; libbdlora is built for sm_100a only", cuda_device, maj, min);
+  return BDLORA_OK;
+}
+
+// ---------------------------------------------------------------------------- comm
+int bdlora_comm_unique_id(uint8_t id[BDLORA_UNIQUE_ID_BYTES]) {
+  if (!id) return fail(BDLORA_E_ARG, "id is NULL");
+  static_assert(sizeof(ncclUniqueId) == BDLORA_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  ncclUniqueId u;
+  NC_TRY(ncclGetUniqueId(&u));
+  memcpy(id, &u, sizeof(u));
+  return BDLORA_OK;
+}
+
+int bdlora_comm_init(const uint8_t id[BDLORA_UNIQUE_ID_BYTES], int nranks, int rank, int cuda_device,
+                     bdlora_comm** out) {
+  if (!id || !out) return fail(BDLORA_E_ARG, "id/out is NULL");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(BDLORA_E_ARG, "bad nranks=%d rank=%d", nranks, rank);
+  ST_TRY(bdlora_device_check(cuda_device));
+  DeviceGuard dg(cuda_device);
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  bdlora_comm* c = new bdlora_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->dev = cuda_device;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(BDLORA_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out = c;
+  return BDLORA_OK;
+}
+
+int bdlora_comm_destroy(bdlora_comm* c) {
+  if (!c) return BDLORA_OK;
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  delete c;
+  return BDLORA_OK;
+}
+
+int bdlora_comm_stats(const bdlora_comm* c, int64_t counts[6]) {
+  if (!c || !counts) return fail(BDLORA_E_ARG, "comm/counts is NULL");
+  memcpy(counts, c->counts, sizeof(c->counts));
+  return BDLORA_OK;
+}
+
+// ---------------------------------------------------------------------------- pool
+int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_pool** out) {
+  if (!desc || !out) return fail(BDLORA_E_ARG, "desc/out is NULL");
+  const bdlora_pool_desc& d = *desc;
+  if (d.parallel != BDLORA_COLUMN && d.parallel != BDLORA_ROW) return fail(BDLORA_E_ARG, "parallel = %d", d.parallel);
+  if (d.sharding != BDLORA_SHARD_BD && d.sharding != BDLORA_SHARD_SLORA)
+    return fail(BDLORA_E_ARG, "sharding = %d", d.sharding);
+  if (d.tp_size < 1 || d.tp_rank < 0 || d.tp_rank >= d.tp_size)
+    return fail(BDLORA_E_ARG, "tp_size = %d, tp_rank = %d", d.tp_size, d.tp_rank);
+  if (d.n_slices < 1 || d.n_slices > BDLORA_MAX_SLICES) return fail(BDLORA_E_ARG, "n_slices = %d", d.n_slices);
+  if (d.parallel == BDLORA_ROW && d.n_slices != 1) return fail(BDLORA_E_ARG, "ROW pools take n_slices = 1 (got %d)", d.n_slices);
+  if (d.d_in <= 0) return fail(BDLORA_E_ARG, "d_in = %d", d.d_in);
+  for (int j = 0; j < d.n_slices; ++j)
+    if (d.d_out[j] <= 0) return fail(BDLORA_E_ARG, "d_out[%d] = %d", j, d.d_out[j]);
+  if (d.capacity < 1 || d.capacity > (1 << 20)) return fail(BDLORA_E_CAPACITY, "capacity = %d", d.capacity);
+  if (d.max_rank < 1 || d.max_rank > 4096) return fail(BDLORA_E_CAPACITY, "max_rank = %d (1..4096)", d.max_rank);
+  if (d.arena_bytes < 0) return fail(BDLORA_E_ARG, "arena_bytes < 0");
+  const int N = d.tp_size;
+  if (d.max_rank % N) return fail(BDLORA_E_DIVISIBILITY, "max_rank %d not divisible by tp_size %d", d.max_rank, N);
+  if (d.parallel == BDLORA_COLUMN) {
+    for (int j = 0; j < d.n_slices; ++j)
+      if (d.d_out[j] % N) return fail(BDLORA_E_DIVISIBILITY, "d_out[%d] = %d not divisible by tp_size %d", j, d.d_out[j], N);
+    if (d.d_in % 8) return fail(BDLORA_E_ARG, "d_in = %d must be a multiple of 8 (128-bit rows)", d.d_in);
+  } else {
+    if (d.d_in % N) return fail(BDLORA_E_DIVISIBILITY, "d_in %d not divisible by tp_size %d", d.d_in, N);
+    if ((d.d_in / N) % 8) return fail(BDLORA_E_ARG, "d_in/N = %d must be a multiple of 8", d.d_in / N);
+    if (d.sharding == BDLORA_SHARD_SLORA && d.d_out[0] % N)
+      return fail(BDLORA_E_DIVISIBILITY, "d_out %d not divisible by tp_size %d (S-LoRA B column shards)", d.d_out[0], N);
+  }
+  ST_TRY(bdlora_device_check(cuda_device));
+  DeviceGuard dg(cuda_device);
+
+  bdlora_pool* p = new bdlora_pool();
+  p->d = d;
+  p->dev = cuda_device;
+  Geom& g = p->g;
+  memset(&g, 0, sizeof(g));
+  const int i = d.tp_rank;
+  if (d.parallel == BDLORA_COLUMN) {
+    g.K = d.d_in;
+    g.J = d.n_slices;
+    int c0 = 0;
+    for (int j = 0; j < g.J; ++j) {
+      const int w = d.d_out[j] / N;
+      g.col0[j] = c0;
+      g.e_lo[j] = c0;
+      g.e_hi[j] = c0 + w;
+      p->ldb[j] = w;
+      c0 += w;
+    }
+    g.col0[g.J] = c0;
+    g.M = c0;
+    g.Rc = d.max_rank / N;
+    g.C = (d.sharding == BDLORA_SHARD_SLORA) ? N : 1;
+    p->rs_max = d.max_rank / N;
+    p->re_max = (d.sharding == BDLORA_SHARD_SLORA) ? d.max_rank : d.max_rank / N;
+  } else {
+    g.K = d.d_in / N;
+    g.J = 1;
+    g.M = d.d_out[0];
+    g.col0[0] = 0;
+    g.col0[1] = g.M;
+    if (d.sharding == BDLORA_SHARD_BD) {
+      g.e_lo[0] = 0;
+      g.e_hi[0] = g.M;
+      p->ldb[0] = g.M;
+      g.Rc = d.max_rank / N;
+      p->rs_max = p->re_max = d.max_rank / N;
+    } else {
+      const int w = g.M / N;
+      g.e_lo[0] = i * w;
+      g.e_hi[0] = (i + 1) * w;
+      p->ldb[0] = w;
+      g.Rc = d.max_rank;
+      p->rs_max = p->re_max = d.max_rank;
+    }
+    g.C = 1;
+  }
+  p->h_tab.assign(d.capacity, SlotEntry{});
+  p->slot_elems.assign(d.capacity, 0);
+  int64_t per_slot = slot_elems_for_rank(p, d.max_rank);
+  if (d.arena_bytes == 0) {
+    p->arena_elems = per_slot * d.capacity;
+    p->ragged = false;
+  } else {
+    p->arena_elems = d.arena_bytes / 2;
+    p->ragged = true;
+    p->free_list[0] = p->arena_elems;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  p->num_sms = sms;
+  cudaError_t e1 = cudaMalloc(&p->arena, std::max<int64_t>(p->arena_elems, 8) * 2);
+  cudaError_t e2 = cudaMalloc(&p->d_tab, sizeof(SlotEntry) * d.capacity);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    if (p->arena) cudaFree(p->arena);
+    if (p->d_tab) cudaFree(p->d_tab);
+    delete p;
+    return fail(BDLORA_E_CUDA, "cudaMalloc arena (%lld B) / table: %s", (long long)(p->arena_elems * 2),
+                cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  }
+  cudaMemset(p->d_tab, 0, sizeof(SlotEntry) * d.capacity);
+  cudaMemset(p->arena, 0, std::max<int64_t>(p->arena_elems, 8) * 2);
+  CU_TRY(cudaDeviceSynchronize());
+  *out = p;
+  return BDLORA_OK;
+}
+
+int bdlora_destroy_pool(bdlora_pool* p) {
+  if (!p) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  cudaFree(p->arena);
+  cudaFree(p->d_tab);
+  delete p;
+  return BDLORA_OK;
+}
+
+static int arena_alloc(bdlora_pool* p, int slot, int64_t elems, int64_t* off) {
+  if (!p->ragged) {
+    *off = slot_elems_for_rank(p, p->d.max_rank) * slot;
+    return BDLORA_OK;
+  }
+  for (auto it = p->free_list.begin(); it != p->free_list.end(); ++it) {
+    if (it->second >= elems) {
+      *off = it->first;
+      const int64_t rest = it->second - elems;
+      const int64_t noff = it->first + elems;
+      p->free_list.erase(it);
+      if (rest > 0) p->free_list[noff] = rest;
+      return BDLORA_OK;
+    }
+  }
+  return fail(BDLORA_E_CAPACITY, "arena full: no free run of %lld elements for slot %d", (long long)elems, slot);
+}
+
+static void arena_free(bdlora_pool* p, int64_t off, int64_t elems) {
+  if (!p->ragged || elems == 0) return;
+  auto it = p->free_list.emplace(off, elems).first;
+  // coalesce with next
+  auto nx = std::next(it);
+  if (nx != p->free_list.end() && it->first + it->second == nx->first) {
+    it->second += nx->second;
+    p->free_list.erase(nx);
+  }
+  if (it != p->free_list.begin()) {
+    auto pv = std::prev(it);
+    if (pv->first + pv->second == it->first) {
+      pv->second += it->second;
+      p->free_list.erase(it);
+    }
+  }
+}
+
+static int gather_to(const uint16_t* src, int64_t ld, int r0, int c0, int nr, int nc, int transpose, uint16_t* dst,
+                     cudaStream_t st) {
+  if (nr == 0 || nc == 0) return BDLORA_OK;
+  dim3 grid((nc + 31) / 32, (nr + 31) / 32);
+  bdl::gather_kernel<<<grid, dim3(32, 8), 0, st>>>(src, ld, r0, c0, nr, nc, transpose, dst);
+  CU_TRY(cudaGetLastError());
+  return BDLORA_OK;
+}
+
+int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale, const void* const* A,
+                        const void* const* B, int32_t src_is_device, bdlora_stream_t stream) {
+  ST_TRY(check_pool(p));
+  const auto& d = p->d;
+  if (slot < 0 || slot >= d.capacity) return fail(BDLORA_E_CAPACITY, "slot %d out of range [0,%d)", slot, d.capacity);
+  if (rank < 1 || rank > d.max_rank) return fail(BDLORA_E_CAPACITY, "rank %d out of range [1,%d]", rank, d.max_rank);
+  const int N = d.tp_size, i = d.tp_rank, J = p->g.J;
+  // BD: rank r/N per shard; S-LoRA column: rank chunks of r/N.  S-LoRA row keeps
+  // the full rank on every device.
+  const bool need_div = !(d.sharding == BDLORA_SHARD_SLORA && d.parallel == BDLORA_ROW);
+  if (need_div && rank % N)
+    return fail(BDLORA_E_DIVISIBILITY, "rank %d not divisible by tp_size %d (P:462)", rank, N);
+  if (!A || !B) return fail(BDLORA_E_ARG, "A/B arrays are NULL");
+  for (int j = 0; j < J; ++j)
+    if (!A[j] || !B[j]) return fail(BDLORA_E_ARG, "A[%d]/B[%d] is NULL", j, j);
+  if (!std::isfinite(scale)) return fail(BDLORA_E_ARG, "scale is not finite");
+  DeviceGuard dg(p->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+
+  // release the previous occupant
+  if (p->h_tab[slot].loaded) bdlora_unload_adapter(p, slot);
+
+  int rs, re;
+  ranks_for(p, rank, &rs, &re);
+  const int64_t elems = slot_elems_for_rank(p, rank);
+  int64_t off = 0;
+  ST_TRY(arena_alloc(p, slot, elems, &off));
+
+  // full source shapes (paper orientation) per mode
+  SlotEntry e{};
+  e.rs = rs;
+  e.re = re;
+  e.scale = scale;
+  e.loaded = 1;
+  const int K = p->g.K;
+  int64_t cur = off;
+  std::vector<void*> staging;
+  auto cleanup = [&]() {
+    for (void* s : staging) cudaFree(s);
+  };
+  auto src_ptr = [&](const void* hsrc, int64_t n_elems, const uint16_t** out) -> int {
+    if (src_is_device) {
+      *out = (const uint16_t*)hsrc;
+      return BDLORA_OK;
+    }
+    void* dp = nullptr;
+    cudaError_t ce = cudaMalloc(&dp, std::max<int64_t>(n_elems, 1) * 2);
+    if (ce != cudaSuccess) return fail(BDLORA_E_CUDA, "staging cudaMalloc: %s", cudaGetErrorString(ce));
+    staging.push_back(dp);
+    ce = cudaMemcpyAsync(dp, hsrc, n_elems * 2, cudaMemcpyHostToDevice, st);
+    if (ce != cudaSuccess) return fail(BDLORA_E_CUDA, "staging copy: %s", cudaGetErrorString(ce));
+    *out = (const uint16_t*)dp;
+    return BDLORA_OK;
+  };
+  int rc = BDLORA_OK;
+  for (int j = 0; j < J && rc == BDLORA_OK; ++j) {
+    const int dout = d.d_out[j];
+    const int w = p->ldb[j];
+    const uint16_t *sa = nullptr, *sb = nullptr;
+    // ---- A_j -> [rs, K] ----
+    if (d.parallel == BDLORA_COLUMN) {
+      // A_j full d_in x r; shard = columns [i*r/N, (i+1)*r/N) (BD and S-LoRA: column-sharded A_1)
+      rc = src_ptr(A[j], (int64_t)d.d_in * rank, &sa);
+      if (rc) break;
+      e.offA[j] = cur;
+      rc = gather_to(sa, rank, 0, i * (rank / N), d.d_in, rank / N, 1, p->arena + cur, st);
+      cur += (int64_t)rs * K;
+    } else if (d.sharding == BDLORA_SHARD_BD) {
+      // A_2 compact d_in x r/N, blocks stacked; diagonal block i = rows [i*d_in/N, ...)
+      rc = src_ptr(A[0], (int64_t)d.d_in * (rank / N), &sa);
+      if (rc) break;
+      e.offA[0] = cur;
+      rc = gather_to(sa, rank / N, i * K, 0, K, rank / N, 1, p->arena + cur, st);
+      cur += (int64_t)rs * K;
+    } else {
+      // S-LoRA row: A_2 d_in x r row-sharded: rows [i*d_in/N, ...)
+      rc = src_ptr(A[0], (int64_t)d.d_in * rank, &sa);
+      if (rc) break;
+      e.offA[0] = cur;
+      rc = gather_to(sa, rank, i * K, 0, K, rank, 1, p->arena + cur, st);
+      cur += (int64_t)rs * K;
+    }
+    if (rc) break;
+    // ---- B_j -> [re, w] ----
+    if (d.parallel == BDLORA_COLUMN && d.sharding == BDLORA_SHARD_BD) {
+      // compact (r/N) x d_out_j, blocks side by side; diagonal block i = columns [i*w, ...)
+      rc = src_ptr(B[j], (int64_t)(rank / N) * dout, &sb);
+      if (rc) break;
+      e.offB[j] = cur;
+      rc = gather_to(sb, dout, 0, i * w, rank / N, w, 0, p->arena + cur, st);
+    } else if (d.parallel == BDLORA_COLUMN) {
+      // S-LoRA column: B_1 r x d_out_j column-sharded
+      rc = src_ptr(B[j], (int64_t)rank * dout, &sb);
+      if (rc) break;
+      e.offB[j] = cur;
+      rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + cur, st);
+    } else if (d.sharding == BDLORA_SHARD_BD) {
+      // BD row: B_2 r x d_out row-sharded: rows [i*r/N, ...)
+      rc = src_ptr(B[0], (int64_t)rank * dout, &sb);
+      if (rc) break;
+      e.offB[0] = cur;
+      rc = gather_to(sb, dout, i * (rank / N), 0, rank / N, dout, 0, p->arena + cur, st);
+    } else {
+      // S-LoRA row: B_2 r x d_out column-sharded
+      rc = src_ptr(B[0], (int64_t)rank * dout, &sb);
+      if (rc) break;
+      e.offB[0] = cur;
+      rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + cur, st);
+    }
+    cur += (int64_t)re * w;
+  }
+  if (rc != BDLORA_OK) {
+    cudaStreamSynchronize(st);
+    cleanup();
+    arena_free(p, off, elems);
+    return rc;
+  }
+  p->h_tab[slot] = e;
+  p->slot_elems[slot] = elems;
+  p->resident_elems += elems;
+  cudaError_t ce = cudaMemcpyAsync(p->d_tab + slot, &p->h_tab[slot], sizeof(SlotEntry), cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);  // host table entry + staging must outlive the copy
+  cleanup();
+  if (ce != cudaSuccess) return fail(BDLORA_E_CUDA, "load_adapter: %s", cudaGetErrorString(ce));
+  (void)off;
+  return BDLORA_OK;
+}
+
+int bdlora_unload_adapter(bdlora_pool* p, int32_t slot) {
+  ST_TRY(check_pool(p));
+  if (slot < 0 || slot >= p->d.capacity) return fail(BDLORA_E_CAPACITY, "slot %d out of range [0,%d)", slot, p->d.capacity);
+  if (!p->h_tab[slot].loaded) return fail(BDLORA_E_NOT_LOADED, "slot %d is not loaded", slot);
+  DeviceGuard dg(p->dev);
+  const SlotEntry e = p->h_tab[slot];
+  const int64_t elems = p->slot_elems[slot];
+  p->h_tab[slot] = SlotEntry{};
+  p->slot_elems[slot] = 0;
+  p->resident_elems -= elems;
+  arena_free(p, e.offA[0], elems);
+  CU_TRY(cudaMemcpy(p->d_tab + slot, &p->h_tab[slot], sizeof(SlotEntry), cudaMemcpyHostToDevice));
+  return BDLORA_OK;
+}
+
+int bdlora_pool_bytes(const bdlora_pool* p, int64_t* resident, int64_t* arena) {
+  ST_TRY(check_pool(p));
+  if (resident) *resident = p->resident_elems * 2;
+  if (arena) *arena = p->arena_elems * 2;
+  return BDLORA_OK;
+}
+
+int bdlora_pool_geometry(const bdlora_pool* p, int32_t* k_loc, int32_t* m_loc) {
+  ST_TRY(check_pool(p));
+  if (k_loc) *k_loc = p->g.K;
+  if (m_loc) *m_loc = p->g.M;
+  return BDLORA_OK;
+}
+
+int bdlora_workspace_bytes(const bdlora_pool* p, int64_t T, size_t* bytes) {
+  ST_TRY(check_pool(p));
+  if (!bytes) return fail(BDLORA_E_ARG, "bytes is NULL");
+  if (T < 0) return fail(BDLORA_E_ARG, "T < 0");
+  *bytes = ws_layout(p, std::max<int64_t>(T, 1)).total;
+  return BDLORA_OK;
+}
+
+int bdlora_v_elems(const bdlora_pool* p, int64_t T, int64_t* elems) {
+  ST_TRY(check_pool(p));
+  if (!elems) return fail(BDLORA_E_ARG, "elems is NULL");
+  *elems = T * p->g.J * p->g.Rc;
+  return BDLORA_OK;
+}
+
+int bdlora_build_segments(const int32_t* ids, int64_t T, int32_t* seg_start, int32_t* seg_len, int32_t* seg_id,
+                          int32_t* n_seg_dev, bdlora_stream_t stream) {
+  if (T < 0) return fail(BDLORA_E_ARG, "T < 0");
+  if (!n_seg_dev) return fail(BDLORA_E_ARG, "n_seg_dev is NULL");
+  if (T > 0 && (!ids || !seg_start || !seg_len || !seg_id)) return fail(BDLORA_E_ARG, "NULL array");
+  if (T > (1 << 24)) return fail(BDLORA_E_CAPACITY, "T too large");
+  bdl::segments_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(ids, (int)T, seg_start, seg_len, seg_id, n_seg_dev);
+  CU_TRY(cudaGetLastError());
+  return BDLORA_OK;
+}
+
+// ---------------------------------------------------------------------------- phases
+int bdlora_lora_shrink(bdlora_pool* p, const void* X, int64_t T, const int32_t* ids, float* v, void* ws,
+                       size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_pool(p));
+  if (T == 0) return BDLORA_OK;
+  if (!X || !ids || !v) return fail(BDLORA_E_ARG, "X/ids/v is NULL");
+  (void)ws;
+  (void)ws_bytes;
+  DeviceGuard dg(p->dev);
+  return launch_shrink(p, X, (int)T, ids, v, (cudaStream_t)stream);
+}
+
+int bdlora_base_expand(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, const float* v,
+                       void* Y, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  if (T == 0) return BDLORA_OK;
+  if (!v) return fail(BDLORA_E_ARG, "v is NULL");
+  DeviceGuard dg(p->dev);
+  return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------- BD-LoRA
+static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y, void* ws,
+                    cudaStream_t st) {
+  float* v = ws_v(p, ws, T);
+  ST_TRY(launch_shrink(p, X, (int)T, ids, v, st));
+  return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st);
+}
+
+int bdlora_column_forward(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y,
+                          void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_COLUMN, BDLORA_SHARD_BD, "bdlora_column_forward"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  return bd_local(p, X, T, W, ids, Y, ws, (cudaStream_t)stream);
+}
+
+int bdlora_row_partial(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* P, void* ws,
+                       size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, P, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_ROW, BDLORA_SHARD_BD, "bdlora_row_partial"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  return bd_local(p, X, T, W, ids, P, ws, (cudaStream_t)stream);
+}
+
+int bdlora_row_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t T, const void* W, const int32_t* ids,
+                       void* Y, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_ROW, BDLORA_SHARD_BD, "bdlora_row_forward"));
+  ST_TRY(require_comm(p, comm, "bdlora_row_forward"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  ST_TRY(bd_local(p, X, T, W, ids, Y, ws, st));
+  if (p->d.tp_size > 1) {
+    // Alg. 1 line 15: the base model's own all-reduce -- the only collective
+    const size_t n = (size_t)T * p->g.M;
+    NC_TRY(ncclAllReduce(Y, Y, n, ncclBfloat16, ncclSum, comm->nccl, st));
+    comm->counts[0] += 1;
+    comm->counts[3] += (int64_t)n * 2;
+  }
+  return BDLORA_OK;
+}
+
+// ---------------------------------------------------------------------------- S-LoRA
+int slora_column_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t T, const void* W,
+                         const int32_t* ids, void* Y, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_COLUMN, BDLORA_SHARD_SLORA, "slora_column_forward"));
+  ST_TRY(require_comm(p, comm, "slora_column_forward"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  float* v = ws_v(p, ws, T);  // [N][T][J][Rc]
+  const size_t chunk = (size_t)T * p->g.J * p->g.Rc;
+  // matmul_3 into this rank's chunk, then the merged all-gather
+  ST_TRY(launch_shrink(p, X, (int)T, ids, v + chunk * p->d.tp_rank, st));
+  if (p->d.tp_size > 1) {
+    NC_TRY(ncclAllGather(v + chunk * p->d.tp_rank, v, chunk, ncclFloat32, comm->nccl, st));
+    comm->counts[1] += 1;
+    comm->counts[4] += (int64_t)chunk * 4;
+  }
+  return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st);
+}
+
+int slora_row_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t T, const void* W, const int32_t* ids,
+                      void* Y, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_ROW, BDLORA_SHARD_SLORA, "slora_row_forward"));
+  ST_TRY(require_comm(p, comm, "slora_row_forward"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  float* v = ws_v(p, ws, T);  // [T][1][Rc = max_rank]
+  ST_TRY(launch_shrink(p, X, (int)T, ids, v, st));
+  if (p->d.tp_size > 1) {
+    // all-reduce after matmul_5
+    const size_t n = (size_t)T * p->g.Rc;
+    NC_TRY(ncclAllReduce(v, v, n, ncclFloat32, ncclSum, comm->nccl, st));
+    comm->counts[2] += 1;
+    comm->counts[5] += (int64_t)n * 4;
+  }
+  ST_TRY(launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st));
+  if (p->d.tp_size > 1) {
+    const size_t n = (size_t)T * p->g.M;
+    NC_TRY(ncclAllReduce(Y, Y, n, ncclBfloat16, ncclSum, comm->nccl, st));
+    comm->counts[0] += 1;
+    comm->counts[3] += (int64_t)n * 2;
+  }
+  return BDLORA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,381 @@
+"""GPU parity of the C-ABI path against the fp64 oracle (SURVEY §8(c) step 7 tolerance:
+max|y - y_ref| <= 2e-2 max|y_ref| and sum|y - y_ref| / sum|y_ref| <= 5e-3), element by element on
+seeded inputs.  TP degrees are emulated on one GPU: every tp_rank's device-local call runs on
+cuda:0 and is compared with the oracle's block for that rank (column) or the oracle's per-rank
+partial and their sum (row).  The S-LoRA collectives are emulated in the test through the
+phase entry points (bdlora_lora_shrink / bdlora_base_expand); the NCCL path itself needs >1 GPU."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import lora as ol
+from tests import _harness as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    bd.bdlora_device_check(0)
+    return torch.device("cuda", 0)
+
+
+def _np(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _assert_tol(y, ref, what):
+    ok, m, l1 = ol.within_tolerance(y, ref)
+    assert ok, f"{what}: max-rel {m:.3e} (<=2e-2), l1-rel {l1:.3e} (<=5e-3)"
+
+
+def run_column(case: H.Case, i: int, dev, fwd="bd"):
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    pool = H.make_pool(case, i)
+    X, W, ids = H.device_inputs(case, i, dev)
+    T = X.shape[0]
+    Y = torch.full((T, pool.m_loc), float("nan"), dtype=torch.bfloat16, device=dev)
+    ws = bd.make_workspace(pool, T)
+    bd.bdlora_column_forward(pool, X, W, ids, Y, ws)
+    torch.cuda.synchronize()
+    pool.close()
+    return Y
+
+
+def run_row_partial(case: H.Case, i: int, dev):
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    pool = H.make_pool(case, i)
+    X, W, ids = H.device_inputs(case, i, dev)
+    T = X.shape[0]
+    P = torch.full((T, pool.m_loc), float("nan"), dtype=torch.bfloat16, device=dev)
+    ws = bd.make_workspace(pool, T)
+    bd.bdlora_row_partial(pool, X, W, ids, P, ws)
+    torch.cuda.synchronize()
+    pool.close()
+    return P
+
+
+# ----------------------------------------------------------------------------- a2: segments
+
+@pytest.mark.parametrize("T", [0, 1, 2, 17, 1024, 1500, 5000])
+def test_segments_bit_exact(dev, T):
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    rng = synth.rng_for(T, 1)
+    ids = synth.ids_runs(rng, T, 5, p_none=0.2, mean_run=3.0) if T else np.zeros(0, np.int32)
+    ss, sl, si, n = bd.bdlora_build_segments(torch.from_numpy(ids).to(dev))
+    torch.cuda.synchronize()
+    n = int(n.item())
+    got = list(zip(ss[:n].tolist(), sl[:n].tolist(), si[:n].tolist()))
+    assert got == ol.segments(ids.tolist())
+
+
+# ----------------------------------------------------------------------------- column BD
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("T", [1, 3, 37])
+def test_column_bd_8b_qkv(dev, n, T):
+    """8B QKV shapes (4096 -> 4096|1024|1024), r=16, mixed ids with -1, every tp_rank."""
+    proj = synth.arch_projections("llama-3.1-8b")[0]
+    case = H.make_case(100 + n * 10 + T, proj, "bd", n, T, ranks=[16, 16, 32])
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", n)
+    for i in range(n):
+        Y = run_column(case, i, dev)
+        _assert_tol(_np(Y), ol.column_device_output(ref_full, n, i), f"N={n} rank {i} T={T}")
+
+
+def test_column_bd_tiny_config0(dev):
+    """configs[0]: tiny column 256 -> 512, r=8, 4 adapters, 16 tokens mixed ids, TP=2."""
+    proj = synth.tiny_pair()[0]
+    ids = np.array([0, 0, 1, 1, 1, 2, 3, 3, 0, 2, 2, 1, 3, 3, 3, 0], np.int32)
+    case = H.make_case(5, proj, "bd", 2, 16, ranks=[8, 8, 8, 8], ids=ids)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", 2)
+    for i in range(2):
+        _assert_tol(_np(run_column(case, i, dev)), ol.column_device_output(ref_full, 2, i), f"rank {i}")
+
+
+@pytest.mark.parametrize("which", ["W0", "A0"])
+def test_column_lora_and_base_isolated(dev, which):
+    """Step 7 (ii) W = 0 isolates the LoRA path; (iii) A = 0 the base path."""
+    proj = synth.arch_projections("llama-3.1-8b")[2]  # gate_up
+    n, T = 4, 9
+    if which == "W0":
+        case = H.make_case(31, proj, "bd", n, T, ranks=[16, 32], w_zero=True)
+    else:
+        case = H.make_case(32, proj, "bd", n, T, ranks=[16, 32], zero={0: "A", 1: "A"})
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", n)
+    for i in range(n):
+        _assert_tol(_np(run_column(case, i, dev)), ol.column_device_output(ref_full, n, i), f"{which} rank {i}")
+
+
+def test_zero_adapter_bit_identical_to_base(dev):
+    """P5: a B = 0 adapter gives output bit-identical to the no-adapter (id -1) output."""
+    import torch
+
+    proj = synth.arch_projections("llama-3.1-8b")[0]
+    T = 8
+    case = H.make_case(41, proj, "bd", 2, T, ranks=[16], ids=np.zeros(T, np.int32), zero={0: "B"})
+    y0 = run_column(case, 1, dev)
+    case.ids = -np.ones(T, np.int32)
+    y1 = run_column(case, 1, dev)
+    assert torch.equal(y0.view(torch.int16), y1.view(torch.int16))
+
+
+# ----------------------------------------------------------------------------- row BD
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("T", [1, 37])
+def test_row_bd_8b_down(dev, n, T):
+    """8B down (14336 -> 4096): per-rank partials vs the oracle's Alg. 1 partial, and their sum
+    (the all-reduce, emulated) vs the unsharded oracle."""
+    proj = synth.arch_projections("llama-3.1-8b")[3]
+    case = H.make_case(200 + n * 10 + T, proj, "bd", n, T, ranks=[16, 32, 16])
+    ads = case.oracle_adapters()
+    acc = None
+    for i in range(n):
+        P = run_row_partial(case, i, dev)
+        _assert_tol(_np(P), ol.row_partial_bd(case.X.f64, case.W.f64, ads, case.ids, n, i), f"N={n} partial {i}")
+        acc = _np(P) if acc is None else acc + _np(P)
+    _assert_tol(acc, ol.row_layer(case.X.f64, case.W.f64, ads, case.ids, "bd", n), f"N={n} sum")
+
+
+def test_row_forward_n1_no_comm(dev):
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.tiny_pair()[1]
+    case = H.make_case(51, proj, "bd", 1, 16, ranks=[8, 8])
+    pool = H.make_pool(case, 0)
+    X, W, ids = H.device_inputs(case, 0, dev)
+    Y = torch.empty(16, pool.m_loc, dtype=torch.bfloat16, device=dev)
+    ws = bd.make_workspace(pool, 16)
+    bd.bdlora_row_forward(pool, None, X, W, ids, Y, ws)
+    torch.cuda.synchronize()
+    _assert_tol(_np(Y), ol.row_layer(case.X.f64, case.W.f64, case.oracle_adapters(), case.ids, "bd", 1), "row N=1")
+
+
+# ----------------------------------------------------------------------------- S-LoRA (phases)
+
+def _slora_column_emulated(case: H.Case, dev):
+    """Every rank: shrink -> (all-gather emulated by concatenating the ranks' v) -> base+expand."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    n = case.n
+    T = len(case.ids)
+    pools = [H.make_pool(case, i) for i in range(n)]
+    vs = []
+    for i, p in enumerate(pools):
+        X, W, ids = H.device_inputs(case, i, dev)
+        v = torch.zeros(bd.bdlora_v_elems(p, T), dtype=torch.float32, device=dev)
+        bd.bdlora_lora_shrink(p, X, ids, v, bd.make_workspace(p, T))
+        vs.append(v)
+    vg = torch.cat(vs)  # [N][T][J][Rc]
+    outs = []
+    for i, p in enumerate(pools):
+        X, W, ids = H.device_inputs(case, i, dev)
+        Y = torch.empty(T, p.m_loc, dtype=torch.bfloat16, device=dev)
+        bd.bdlora_base_expand(p, X, W, ids, vg, Y, bd.make_workspace(p, T))
+        outs.append(Y)
+    torch.cuda.synchronize()
+    for p in pools:
+        p.close()
+    return outs, vg
+
+
+@pytest.mark.parametrize("n", [1, 2, 8])
+def test_slora_column_8b_qkv(dev, n):
+    proj = synth.arch_projections("llama-3.1-8b")[0]
+    T = 13
+    case = H.make_case(300 + n, proj, "slora", n, T, ranks=[16, 32, 16])
+    ads = case.oracle_adapters()
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, ads, case.ids, "slora", n)
+    outs, vg = _slora_column_emulated(case, dev)
+    for i in range(n):
+        _assert_tol(_np(outs[i]), ol.column_device_output(ref_full, n, i), f"slora col N={n} rank {i}")
+    # the all-gathered intermediate equals X A (full rank) within fp32 accumulation (step 6)
+    J, Rc = len(proj.d_out), case.max_rank // n
+    v = vg.cpu().numpy().reshape(n, T, J, Rc)
+    for j in range(J):
+        refv = ol.slora_column_gathered_v(case.X.f64, ads, case.ids, j)
+        for t, vec in refv.items():
+            r = ads[int(case.ids[t])]["rank"]
+            got = np.concatenate([v[c, t, j, :r // n] for c in range(n)])
+            assert np.allclose(got, vec, rtol=1e-4, atol=1e-4 * np.abs(vec).max())
+
+
+@pytest.mark.parametrize("n", [1, 2, 8])
+def test_slora_row_8b_o(dev, n):
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.arch_projections("llama-3.1-8b")[1]
+    T = 11
+    case = H.make_case(400 + n, proj, "slora", n, T, ranks=[16, 32])
+    ads = case.oracle_adapters()
+    pools = [H.make_pool(case, i) for i in range(n)]
+    v = None
+    for i, p in enumerate(pools):
+        X, W, ids = H.device_inputs(case, i, dev)
+        vi = torch.zeros(bd.bdlora_v_elems(p, T), dtype=torch.float32, device=dev)
+        bd.bdlora_lora_shrink(p, X, ids, vi, bd.make_workspace(p, T))
+        v = vi if v is None else v + vi  # all-reduce after matmul_5, emulated
+    acc = None
+    for i, p in enumerate(pools):
+        X, W, ids = H.device_inputs(case, i, dev)
+        P = torch.empty(T, p.m_loc, dtype=torch.bfloat16, device=dev)
+        bd.bdlora_base_expand(p, X, W, ids, v, P, bd.make_workspace(p, T))
+        acc = P.float() if acc is None else acc + P.float()  # base all-reduce, emulated
+    torch.cuda.synchronize()
+    _assert_tol(acc.cpu().numpy(), ol.row_layer(case.X.f64, case.W.f64, ads, case.ids, "slora", n), f"slora row N={n}")
+    for p in pools:
+        p.close()
+
+
+# ----------------------------------------------------------------------------- P10 integer mode
+
+@pytest.mark.parametrize("sharding", ["bd", "slora"])
+@pytest.mark.parametrize("n", [1, 4])
+def test_integer_mode_bit_exact_column(dev, sharding, n):
+    """P10: {-1,0,1} inputs, s a power of two: every partial sum is exact, so the GPU output must be
+    bit-identical to the oracle rounded once to bf16, for every rank; routing errors show up
+    through each adapter's B signature."""
+    proj = synth.Projection("qkv", "column", 1024, (512, 256, 256))
+    T = 21
+    case = H.make_case(500 + n, proj, sharding, n, T, ranks=[8, 16, 8, 32], integer=True)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, sharding, n)
+    if sharding == "bd":
+        outs = [run_column(case, i, dev) for i in range(n)]
+    else:
+        outs, _ = _slora_column_emulated(case, dev)
+    for i in range(n):
+        ref = ol.bf16_round(ol.column_device_output(ref_full, n, i))
+        got = _np(outs[i])
+        assert np.array_equal(got, ref), f"rank {i}: {np.count_nonzero(got != ref)} mismatches"
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_integer_mode_bit_exact_row_partials(dev, n):
+    proj = synth.Projection("down", "row", 1024, (512,))
+    T = 19
+    case = H.make_case(600 + n, proj, "bd", n, T, ranks=[8, 16, 32], integer=True)
+    ads = case.oracle_adapters()
+    for i in range(n):
+        ref = ol.bf16_round(ol.row_partial_bd(case.X.f64, case.W.f64, ads, case.ids, n, i))
+        got = _np(run_row_partial(case, i, dev))
+        assert np.array_equal(got, ref), f"rank {i}: {np.count_nonzero(got != ref)} mismatches"
+
+
+# ----------------------------------------------------------------------------- multi-tenant / pool
+
+def test_multitenant_mixed_ranks_ragged_arena(dev):
+    """C4-like: 16 resident adapters r in {8,16,32,64,128}, uniform ids over them, T=64, TP=8
+    (70B-gate_up-like but narrower), ragged arena with unload / reload."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.Projection("gate_up", "column", 2048, (3584, 3584))
+    n, T = 8, 64
+    ranks = [[8, 16, 32, 64, 128][k % 5] for k in range(16)]
+    rng = synth.rng_for(7, 7)
+    ids = synth.ids_uniform(rng, T, 16)
+    case = H.make_case(700, proj, "bd", n, T, ranks=ranks, ids=ids)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", n)
+    i = 5
+    pool = H.make_pool(case, i, arena_bytes=64 << 20)
+    # unload + reload a few slots to exercise the ragged allocator
+    for a in (3, 7, 11):
+        bd.bdlora_unload_adapter(pool, a)
+    for a in (11, 3, 7):
+        ad = case.adapters[a]
+        bd.bdlora_load_adapter(pool, a, ad.rank, ad.scale, [H.torch_bf16(x.bits) for x in ad.A],
+                               [H.torch_bf16(x.bits) for x in ad.B])
+    X, W, idt = H.device_inputs(case, i, dev)
+    Y = torch.empty(T, pool.m_loc, dtype=torch.bfloat16, device=dev)
+    bd.bdlora_column_forward(pool, X, W, idt, Y, bd.make_workspace(pool, T))
+    torch.cuda.synchronize()
+    _assert_tol(_np(Y), ol.column_device_output(ref_full, n, i), "multi-tenant")
+    res, arena = bd.bdlora_pool_bytes(pool)
+    assert 0 < res <= arena
+    pool.close()
+
+
+def test_device_resident_factor_loading(dev):
+    """Loading from device pointers gives the same result as from host pointers."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.tiny_pair()[1]
+    case = H.make_case(61, proj, "bd", 2, 16, ranks=[8, 8])
+    p_host = H.make_pool(case, 1)
+    p_dev = bd.bdlora_create_pool(bd.ROW, bd.SHARD_BD, 2, 1, proj.d_in, proj.d_out, 2, 8)
+    for a, ad in case.adapters.items():
+        bd.bdlora_load_adapter(p_dev, a, ad.rank, ad.scale, [H.torch_bf16(x.bits, dev) for x in ad.A],
+                               [H.torch_bf16(x.bits, dev) for x in ad.B])
+    X, W, ids = H.device_inputs(case, 1, dev)
+    outs = []
+    for p in (p_host, p_dev):
+        P = torch.empty(16, p.m_loc, dtype=torch.bfloat16, device=dev)
+        bd.bdlora_row_partial(p, X, W, ids, P, bd.make_workspace(p, 16))
+        outs.append(P)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    p_host.close()
+    p_dev.close()
+
+
+# ----------------------------------------------------------------------------- errors / edge cases
+
+def test_error_paths(dev):
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.tiny_pair()[0]
+    case = H.make_case(71, proj, "bd", 2, 4, ranks=[8])
+    pool = H.make_pool(case, 0)
+    X, W, ids = H.device_inputs(case, 0, dev)
+    Y = torch.empty(4, pool.m_loc, dtype=torch.bfloat16, device=dev)
+    ws = bd.make_workspace(pool, 4)
+    with pytest.raises(bd.BdloraError) as e:
+        bd.slora_column_forward(pool, None, X, W, ids, Y, ws)
+    assert e.value.code == 5
+    with pytest.raises(bd.BdloraError) as e:
+        bd.bdlora_row_partial(pool, X, W, ids, Y, ws)
+    assert e.value.code == 5
+    with pytest.raises(bd.BdloraError) as e:
+        bd.bdlora_column_forward(pool, X, W, ids, Y, ws[:128])
+    assert e.value.code == 1
+    a = case.adapters[0]
+    with pytest.raises(bd.BdloraError) as e:
+        bd.bdlora_load_adapter(pool, 0, 16, 1.0, [H.torch_bf16(x.bits) for x in a.A], [H.torch_bf16(x.bits) for x in a.B])
+    assert e.value.code == 3  # rank > max_rank
+    with pytest.raises(bd.BdloraError) as e:
+        bd.bdlora_load_adapter(pool, 5, 8, 1.0, [H.torch_bf16(x.bits) for x in a.A], [H.torch_bf16(x.bits) for x in a.B])
+    assert e.value.code == 3  # slot out of range
+    with pytest.raises(bd.BdloraError) as e:
+        bd.bdlora_load_adapter(pool, 0, 6, 1.0, [H.torch_bf16(x.bits) for x in a.A], [H.torch_bf16(x.bits) for x in a.B])
+    assert e.value.code == 2  # N does not divide r
+    with pytest.raises(bd.BdloraError) as e:
+        bd.bdlora_unload_adapter(pool, 0) or bd.bdlora_unload_adapter(pool, 0)
+    assert e.value.code == 4
+    # T = 0 is a no-op
+    bd.bdlora_column_forward(pool, X[:0], W, ids[:0], Y[:0], ws)
+    pool.close()
