@@ -91,6 +91,9 @@ int bdlora_abi_version(void);
 const char* bdlora_last_error(void); /* thread-local, never NULL; "" when no error            */
 /* BDLORA_OK iff `cuda_device` is sm_100 (CC 10.0) and the library's kernels can run on it.     */
 int bdlora_device_check(int cuda_device);
+/* Number of kernels this library has enqueued since it was loaded (host-side count of launches;
+   a CUDA-graph replay re-runs the captured launches without counting them again).              */
+int bdlora_kernel_launches(int64_t* n);
 
 /* ---------------------------------------------------------------- communicator (NCCL) ------- */
 /* NCCL 2.28 over NVLink/NVSwitch.  Bootstrap: rank 0 calls bdlora_comm_unique_id, the caller

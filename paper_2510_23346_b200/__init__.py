@@ -22,7 +22,7 @@ SHARD_BD, SHARD_SLORA = 0, 1
 
 __all__ = [
     "COLUMN", "ROW", "SHARD_BD", "SHARD_SLORA", "BdloraError", "Pool", "Comm",
-    "bdlora_abi_version", "bdlora_device_check", "bdlora_comm_unique_id", "bdlora_comm_init",
+    "bdlora_abi_version", "bdlora_device_check", "bdlora_kernel_launches", "bdlora_comm_unique_id", "bdlora_comm_init",
     "bdlora_comm_destroy", "bdlora_comm_stats", "bdlora_create_pool", "bdlora_destroy_pool",
     "bdlora_load_adapter", "bdlora_unload_adapter", "bdlora_pool_bytes", "bdlora_pool_geometry",
     "bdlora_workspace_bytes", "bdlora_build_segments", "bdlora_column_forward", "bdlora_row_partial",
@@ -116,6 +116,12 @@ def bdlora_abi_version() -> int:
 
 def bdlora_device_check(device: int = 0) -> None:
     call("bdlora_device_check", device)
+
+
+def bdlora_kernel_launches() -> int:
+    n = ctypes.c_int64()
+    call("bdlora_kernel_launches", ctypes.byref(n))
+    return n.value
 
 
 # ------------------------------------------------------------------------------------------ comm

@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -67,6 +68,9 @@ struct DeviceGuard {
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+std::atomic<int64_t> g_launches{0};
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 }  // namespace
 
@@ -185,6 +189,7 @@ int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids
   const size_t smem = sizeof(int) * (size_t)T;
   bdl::shrink_kernel<4><<<grid, 256, smem, st>>>((const __nv_bfloat16*)X, T, ids, p->d_tab,
                                                  (const __nv_bfloat16*)p->arena, g, v);
+  count_launch();
   CU_TRY(cudaGetLastError());
   return BDLORA_OK;
 }
@@ -224,6 +229,7 @@ int launch_gemv(const bdlora_pool* p, const void* X, int T, const void* W, const
     default: GEMV_CASE(8); break;
   }
 #undef GEMV_CASE
+  count_launch();
   CU_TRY(cudaGetLastError());
   return BDLORA_OK;
 }
@@ -237,6 +243,7 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
                               (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
                               p->num_sms, st);
     if (rc == 0) {
+      count_launch();
       CU_TRY(cudaGetLastError());
       return BDLORA_OK;
     }
@@ -271,6 +278,12 @@ int require_comm(const bdlora_pool* p, const bdlora_comm* c, const char* fn) {
 extern "C" {
 
 int bdlora_abi_version(void) { return BDLORA_ABI_VERSION; }
+
+int bdlora_kernel_launches(int64_t* n) {
+  if (!n) return fail(BDLORA_E_ARG, "n is NULL");
+  *n = g_launches.load();
+  return BDLORA_OK;
+}
 
 const char* bdlora_last_error(void) { return g_err.c_str(); }
 
@@ -489,6 +502,7 @@ static int gather_to(const uint16_t* src, int64_t ld, int r0, int c0, int nr, in
   if (nr == 0 || nc == 0) return BDLORA_OK;
   dim3 grid((nc + 31) / 32, (nr + 31) / 32);
   bdl::gather_kernel<<<grid, dim3(32, 8), 0, st>>>(src, ld, r0, c0, nr, nc, transpose, dst);
+  count_launch();
   CU_TRY(cudaGetLastError());
   return BDLORA_OK;
 }
@@ -672,6 +686,7 @@ int bdlora_build_segments(const int32_t* ids, int64_t T, int32_t* seg_start, int
   if (T > 0 && (!ids || !seg_start || !seg_len || !seg_id)) return fail(BDLORA_E_ARG, "NULL array");
   if (T > (1 << 24)) return fail(BDLORA_E_CAPACITY, "T too large");
   bdl::segments_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(ids, (int)T, seg_start, seg_len, seg_id, n_seg_dev);
+  count_launch();
   CU_TRY(cudaGetLastError());
   return BDLORA_OK;
 }

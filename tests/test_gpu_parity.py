@@ -371,7 +371,7 @@ def test_error_paths(dev):
         bd.bdlora_load_adapter(pool, 5, 8, 1.0, [H.torch_bf16(x.bits) for x in a.A], [H.torch_bf16(x.bits) for x in a.B])
     assert e.value.code == 3  # slot out of range
     with pytest.raises(bd.BdloraError) as e:
-        bd.bdlora_load_adapter(pool, 0, 6, 1.0, [H.torch_bf16(x.bits) for x in a.A], [H.torch_bf16(x.bits) for x in a.B])
+        bd.bdlora_load_adapter(pool, 0, 7, 1.0, [H.torch_bf16(x.bits) for x in a.A], [H.torch_bf16(x.bits) for x in a.B])
     assert e.value.code == 2  # N does not divide r
     with pytest.raises(bd.BdloraError) as e:
         bd.bdlora_unload_adapter(pool, 0) or bd.bdlora_unload_adapter(pool, 0)
