@@ -136,6 +136,90 @@ __global__ void __launch_bounds__(256) shrink_kernel(const __nv_bfloat16* __rest
 }
 
 // ------------------------------------------------------------------------------------------------
+// Shrink, latency-optimised (decode): one CTA of 128 threads per (first token of an adapter group,
+// slice j, rank row k); the K reduction is spread over all 128 threads (4 independent 128-bit loads
+// in flight per thread for K = 4096) and reduced through shared memory in a fixed order
+// (deterministic).  Signals programmatic dependents immediately so the base GEMM that consumes v can
+// start streaming its weights while this runs.
+// ------------------------------------------------------------------------------------------------
+template <int MT>
+__global__ void __launch_bounds__(128) shrink_rows_kernel(const __nv_bfloat16* __restrict__ X, int T,
+                                                          const int* __restrict__ ids,
+                                                          const SlotEntry* __restrict__ tab,
+                                                          const __nv_bfloat16* __restrict__ arena, Geom g,
+                                                          float* __restrict__ v) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ int s_members[];  // [T]
+  __shared__ int s_cnt, s_dup;
+  __shared__ float s_red[4][MT];
+  const int t = blockIdx.x, j = blockIdx.y, k = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a = __ldg(ids + t);
+  if (a < 0) return;
+  const SlotEntry e = tab[a];
+  if (k >= e.rs || j >= g.J) return;
+  if (warp == 0) {
+    int cnt = 0, dup = 0;
+    for (int base = 0; base < T; base += 32) {
+      const int u = base + lane;
+      const int idu = (u < T) ? __ldg(ids + u) : -2;
+      const unsigned m = __ballot_sync(0xffffffffu, idu == a);
+      if (u < T && idu == a) {
+        if (u < t) dup = 1;
+        s_members[cnt + __popc(m & ((1u << lane) - 1u))] = u;
+      }
+      cnt += __popc(m);
+      if (__any_sync(0xffffffffu, dup)) break;  // not the group leader: stop early
+    }
+    dup = __any_sync(0xffffffffu, dup);
+    if (lane == 0) {
+      s_cnt = cnt;
+      s_dup = dup;
+    }
+  }
+  __syncthreads();
+  if (s_dup) return;
+  const int K = g.K;
+  const __nv_bfloat16* Ar = arena + e.offA[j] + (size_t)k * K;
+  const int cnt = s_cnt;
+  for (int m0 = 0; m0 < cnt; m0 += MT) {
+    float acc[MT];
+    int tok[MT];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      acc[m] = 0.f;
+      tok[m] = (m0 + m < cnt) ? s_members[m0 + m] : -1;
+    }
+#pragma unroll 4
+    for (int d = threadIdx.x * 8; d < K; d += 128 * 8) {
+      float af[8];
+      bf16x8_to_f32(ld_cached_u4(Ar + d), af);
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        if (tok[m] >= 0) {
+          float xf[8];
+          bf16x8_to_f32(ld_cached_u4(X + (size_t)tok[m] * K + d), xf);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[m] = fmaf(af[q], xf[q], acc[m]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const float s = warp_sum(acc[m]);
+      if (lane == 0) s_red[warp][m] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < MT && tok[threadIdx.x] >= 0) {
+      const int m = threadIdx.x;
+      const float s = (s_red[0][m] + s_red[1][m]) + (s_red[2][m] + s_red[3][m]);
+      v[((size_t)tok[m] * g.J + j) * g.Rc + k] = e.scale * s;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Base GEMV + fused LoRA expand (decode, small T).
 // Grid (ntiles, S): CTA = 8 warps x RW output rows = 8*RW rows of W^T; split s covers K range
 // [s*Kc, min(K,(s+1)*Kc)).  S == 1: direct epilogue.  S > 1: partials to part[s][t][n] (plain

@@ -1,13 +1,360 @@
-// kernels_umma.cuh -- tcgen05 / TMA / TMEM base GEMM with the fused LoRA epilogue (sm_100a).
-// (placeholder until the tensor-core path lands: nothing is eligible yet)
+// kernels_umma.cuh -- the base GEMM of both projection kinds (matmul_1 / matmul_2) on the 5th-gen
+// tensor cores, with the LoRA expand + add (matmul_4/6, add_1/2) fused into its epilogue (sm_100a).
+//
+// Swap-AB formulation (decode-friendly): D[n, t] = sum_k W^T[n, k] X[t, k], i.e. the MMA's M dim runs
+// over 128 output columns n (rows of W^T, K-major) and its N dim over BN tokens (X rows, K-major).
+// T = 1 decode pads the token dim to 16 -- the MMA is ~free, the kernel is a TMA weight stream.
+//
+//   warp 0      : TMA producer   -- W tile [128 x 64] + X tile [BN x 64] per stage, SWIZZLE_128B,
+//                                   W with L2 evict_first (read once), X evict_last (re-read)
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer, double-buffered accumulator
+//   warps 2..5  : epilogue       -- tcgen05.ld (thread = output column, registers = tokens),
+//                                   + s_a v B[a] (fp32), one bf16 RNE rounding, store
+//
+// Work split: stream-K over units u = (token tile, 128-row tile, 64-wide k-block); CTA c owns
+// [c U / G, (c+1) U / G) -- perfectly balanced over the G = #SM persistent CTAs for any shape.
+// A tile split between CTAs is finished deterministically: every contributor writes its fp32
+// partial, the CTA completing the tile's k-block count sums the partials in CTA order.
+// The LoRA intermediate v is produced by the shrink kernel launched just before; with programmatic
+// dependent launch the W stream of this kernel overlaps it and only the epilogue waits for it.
 #pragma once
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace bdl {
-inline size_t umma_workspace_bytes(int M, int T) { (void)M; (void)T; return 0; }
-inline bool umma_eligible(const Geom& g, int T) { (void)g; (void)T; return false; }
-inline int umma_launch(const Geom&, const __nv_bfloat16*, int, const __nv_bfloat16*, const int*, const SlotEntry*,
-                       const __nv_bfloat16*, const float*, __nv_bfloat16*, void*, int, cudaStream_t) {
-  return 1;
+
+constexpr int kUmmaBM = 128;
+constexpr int kUmmaBK = 64;
+constexpr int kUmmaThreads = 192;
+
+struct UmmaParams {
+  int M, K, T;
+  int m_tiles, n_tiles, k_blocks;
+  int units, grid;
+  const int* ids;
+  const SlotEntry* tab;
+  const __nv_bfloat16* arena;
+  Geom g;
+  const float* v;
+  __nv_bfloat16* Y;
+  float* part;    // [grid][2][BN][128]
+  int* tile_cnt;  // [m_tiles * n_tiles], zero between launches
+  int pdl;
+};
+
+__device__ __forceinline__ int umma_u_lo(long long c, int units, int grid) { return (int)(c * units / grid); }
+__device__ __forceinline__ int umma_cta_of(long long u, int units, int grid) {
+  // largest c with floor(c*U/G) <= u
+  return (int)(((u + 1) * grid + units - 1) / units) - 1;
 }
+
+template <int BN>
+struct UmmaSmem {
+  static constexpr int kWBytes = kUmmaBM * kUmmaBK * 2;  // 16 KB
+  static constexpr int kXBytes = BN * kUmmaBK * 2;
+  static constexpr int kStageBytes = kWBytes + kXBytes;
+  static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4);
+  static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int kBarOff = kStages * kStageBytes;
+  static constexpr int kBytes = kBarOff + 256 + 1024;  // + barriers/flags + alignment slack
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kUmmaThreads, 1)
+    umma_lora_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                          const UmmaParams p) {
+  using S = UmmaSmem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + S::kStages * S::kWBytes;
+  uint64_t* full = (uint64_t*)(smem + S::kBarOff);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* tfull = empty + S::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
+  int* s_last = (int*)(tmem_holder + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const int u_lo = umma_u_lo(cta, p.units, p.grid);
+  const int u_hi = umma_u_lo(cta + 1, p.units, p.grid);
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmW);
+    ptx::tma_prefetch_desc(&tmX);
+    for (int s = 0; s < S::kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 128);
+    }
+    ptx::fence_mbar_init();
+    ptx::fence_proxy_async();
+  }
+  if (warp == 1) ptx::tmem_alloc<S::kTmemCols>(tmem_holder);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (ptx::elect_one()) {
+      const uint64_t pol_w = ptx::policy_evict_first();
+      const uint64_t pol_x = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = u_lo; u < u_hi;) {
+        const int tile = u / p.k_blocks;
+        const int kb0 = u - tile * p.k_blocks;
+        const int kb1 = min(p.k_blocks, kb0 + (u_hi - u));
+        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+          ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
+          ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        u += kb1 - kb0;
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (ptx::elect_one()) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kUmmaBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = u_lo; u < u_hi;) {
+        const int tile = u / p.k_blocks;
+        const int kb0 = u - tile * p.k_blocks;
+        const int kb1 = min(p.k_blocks, kb0 + (u_hi - u));
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint64_t a_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sW + stage * S::kWBytes));
+          const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sX + stage * S::kXBytes));
+#pragma unroll
+          for (int k = 0; k < kUmmaBK / 16; ++k)  // UMMA_K = 16 bf16 = 32 B -> +2 in the >>4 address field
+            ptx::mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == S::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        u += kb1 - kb0;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;  // TMEM lane quarter accessible by this warp
+    const int row = q * 32 + lane;
+    const int etid = threadIdx.x - 64;  // 0..127
+    if (p.pdl) ptx::pdl_wait();         // v (shrink output) is complete and visible
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = u_lo; u < u_hi;) {
+      const int tile = u / p.k_blocks;
+      const int kb0 = u - tile * p.k_blocks;
+      const int kb1 = min(p.k_blocks, kb0 + (u_hi - u));
+      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int n = mt * kUmmaBM + row;
+      const int t0 = nt * BN;
+      const int tv = min(BN, p.T - t0);
+      const bool whole = (kb0 == 0 && kb1 == p.k_blocks);
+      const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
+      float* my_part = p.part + ((size_t)(cta * 2 + slot) * BN) * kUmmaBM;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      for (int c0 = 0; c0 < tv; c0 += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld_32x32b_x16(taddr + c0, r);
+        ptx::tmem_ld_wait();
+        if (whole) {
+          if (n < p.M) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int t = t0 + c0 + i;
+              if (c0 + i < tv) {
+                const int a = __ldg(p.ids + t);
+                const float y = __uint_as_float(r[i]) + lora_expand_term(t, n, a, p.tab, p.arena, p.g, p.v, p.T);
+                p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y);
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < tv) my_part[(size_t)(c0 + i) * kUmmaBM + row] = __uint_as_float(r[i]);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
+      if (!whole) {
+        ptx::named_bar_sync(1, 128);
+        if (etid == 0) {
+          __threadfence();
+          const int got = kb1 - kb0;
+          const int old = atomicAdd(p.tile_cnt + tile, got);
+          *s_last = (old + got == p.k_blocks);
+        }
+        ptx::named_bar_sync(1, 128);
+        if (*s_last) {
+          __threadfence();
+          const int ts = tile * p.k_blocks;
+          const int c_first = umma_cta_of(ts, p.units, p.grid);
+          const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
+          if (n < p.M) {
+            for (int i = 0; i < tv; ++i) {
+              const int t = t0 + i;
+              float y = 0.f;
+              for (int c = c_first; c <= c_last; ++c) {
+                const int sl = (ts > umma_u_lo(c, p.units, p.grid)) ? 1 : 0;
+                y += __ldcg(p.part + ((size_t)(c * 2 + sl) * BN + i) * kUmmaBM + row);
+              }
+              const int a = __ldg(p.ids + t);
+              y += lora_expand_term(t, n, a, p.tab, p.arena, p.g, p.v, p.T);
+              p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y);
+            }
+          }
+          if (etid == 0) p.tile_cnt[tile] = 0;
+        }
+        ptx::named_bar_sync(1, 128);  // s_last reused by the next segment
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+      u += kb1 - kb0;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == 1) ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Host side
+// ------------------------------------------------------------------------------------------------
+inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
+
+inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
+  const int BN = umma_bn_for(T);
+  const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM;
+  const int n_tiles = (T + BN - 1) / BN;
+  size_t part = (size_t)num_sms * 2 * BN * kUmmaBM * sizeof(float);
+  size_t cnt = (size_t)m_tiles * n_tiles * sizeof(int);
+  return ((cnt + 255) / 256) * 256 + part;
+}
+
+inline bool umma_eligible(const Geom& g, int T) { return T >= 1 && g.K % kUmmaBK == 0 && g.K >= kUmmaBK; }
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_encodeTiled)ptr;
+  }
+  return fn;
+}
+
+// 2D bf16 K-major tensor [rows, K] with box [box_rows, 64], SWIZZLE_128B, OOB -> zeros.
+inline bool encode_kmajor(CUtensorMap* m, const void* base, int K, int rows, int box_rows) {
+  PFN_encodeTiled enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kUmmaBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN>
+inline int umma_launch_bn(const UmmaParams& p0, const __nv_bfloat16* X, const __nv_bfloat16* W, cudaStream_t st) {
+  using S = UmmaSmem<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) !=
+        cudaSuccess)
+      return 2;
+    attr_set = true;
+  }
+  CUtensorMap tmW, tmX;
+  if (!encode_kmajor(&tmW, W, p0.K, p0.M, kUmmaBM)) return 3;
+  if (!encode_kmajor(&tmX, X, p0.K, p0.T, BN)) return 3;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p0.grid);
+  cfg.blockDim = dim3(kUmmaThreads);
+  cfg.dynamicSmemBytes = S::kBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = p0.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN>, tmW, tmX, p0) != cudaSuccess) return 4;
+  return 0;
+}
+
+// Returns 0 on launch, non-zero if the shape is not handled here.
+inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_bfloat16* W, const int* ids,
+                       const SlotEntry* tab, const __nv_bfloat16* arena, const float* v, __nv_bfloat16* Y, void* ws,
+                       int num_sms, cudaStream_t st, int pdl = 0) {
+  if (!umma_eligible(g, T)) return 1;
+  const int BN = umma_bn_for(T);
+  UmmaParams p;
+  p.M = g.M;
+  p.K = g.K;
+  p.T = T;
+  p.m_tiles = (g.M + kUmmaBM - 1) / kUmmaBM;
+  p.n_tiles = (T + BN - 1) / BN;
+  p.k_blocks = (g.K + kUmmaBK - 1) / kUmmaBK;
+  const long long units = (long long)p.m_tiles * p.n_tiles * p.k_blocks;
+  if (units > (1LL << 30)) return 1;
+  p.units = (int)units;
+  p.grid = (int)std::min<long long>(units, num_sms);
+  p.ids = ids;
+  p.tab = tab;
+  p.arena = arena;
+  p.g = g;
+  p.v = v;
+  p.Y = Y;
+  const size_t cnt_bytes = (((size_t)p.m_tiles * p.n_tiles * sizeof(int)) + 255) / 256 * 256;
+  p.tile_cnt = (int*)ws;
+  p.part = (float*)((char*)ws + cnt_bytes);
+  p.pdl = pdl;
+  switch (BN) {
+    case 16: return umma_launch_bn<16>(p, X, W, st);
+    case 32: return umma_launch_bn<32>(p, X, W, st);
+    case 64: return umma_launch_bn<64>(p, X, W, st);
+    case 128: return umma_launch_bn<128>(p, X, W, st);
+    default: return umma_launch_bn<256>(p, X, W, st);
+  }
+}
+
 }  // namespace bdl

@@ -155,7 +155,7 @@ WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   L.off_part = o;
   o = align_up(o + sizeof(float) * (size_t)kPartTokenSplits * p->g.M, 256);
   L.off_umma = o;
-  o = align_up(o + bdl::umma_workspace_bytes(p->g.M, (int)T), 256);
+  o = align_up(o + bdl::umma_workspace_bytes(p->g.M, (int)T, p->num_sms), 256);
   L.total = o;
   return L;
 }
@@ -185,10 +185,11 @@ int check_fwd_args(const bdlora_pool* p, const void* X, int64_t T, const void* W
 int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids, float* v, cudaStream_t st) {
   if (T == 0) return BDLORA_OK;
   const Geom& g = p->g;
-  dim3 grid(T, g.J, (p->rs_max + 7) / 8);
+  if (T > 65535 * 16) return fail(BDLORA_E_CAPACITY, "T = %d too large for the shrink grid", T);
+  dim3 grid(T, g.J, p->rs_max);
   const size_t smem = sizeof(int) * (size_t)T;
-  bdl::shrink_kernel<4><<<grid, 256, smem, st>>>((const __nv_bfloat16*)X, T, ids, p->d_tab,
-                                                 (const __nv_bfloat16*)p->arena, g, v);
+  bdl::shrink_rows_kernel<4><<<grid, 128, smem, st>>>((const __nv_bfloat16*)X, T, ids, p->d_tab,
+                                                      (const __nv_bfloat16*)p->arena, g, v);
   count_launch();
   CU_TRY(cudaGetLastError());
   return BDLORA_OK;
@@ -235,13 +236,13 @@ int launch_gemv(const bdlora_pool* p, const void* X, int T, const void* W, const
 }
 
 int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W, const int32_t* ids, const float* v,
-                       void* Y, void* ws, cudaStream_t st) {
+                       void* Y, void* ws, cudaStream_t st, int pdl = 0) {
   if (T == 0) return BDLORA_OK;
   if (bdl::umma_eligible(p->g, T)) {
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, T, (const __nv_bfloat16*)W, ids, p->d_tab,
                               (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
-                              p->num_sms, st);
+                              p->num_sms, st, pdl);
     if (rc == 0) {
       count_launch();
       CU_TRY(cudaGetLastError());
@@ -717,7 +718,8 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
                     cudaStream_t st) {
   float* v = ws_v(p, ws, T);
   ST_TRY(launch_shrink(p, X, (int)T, ids, v, st));
-  return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st);
+  // programmatic dependent launch: the GEMM streams W while the shrink runs; only its epilogue waits
+  return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st, /*pdl=*/1);
 }
 
 int bdlora_column_forward(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y,
