@@ -86,13 +86,26 @@ __device__ __forceinline__ float lora_expand_term(int t, int n, int a, const Slo
   const int col = n - g.e_lo[j];
   const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + e.offB[j]);
   const int rc = e.re / g.C;
-  float s = 0.f;
+  // 8 independent partial sums -> 16 loads in flight per thread (latency-bound: v is L2-resident,
+  // B rows are read coalesced across the warp's consecutive output columns)
+  float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int c = 0; c < g.C; ++c) {
     const float* vv = v + ((size_t)(c * T + t) * g.J + j) * g.Rc;
     const uint16_t* Bc = B + (size_t)(c * rc) * ldb + col;
-    for (int k = 0; k < rc; ++k) s = fmaf(vv[k], bf16_bits_to_f32(__ldg(Bc + (size_t)k * ldb)), s);
+    int k = 0;
+    for (; k + 8 <= rc; k += 8) {
+      float vk[8], bk[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        vk[q] = __ldg(vv + k + q);
+        bk[q] = bf16_bits_to_f32(__ldg(Bc + (size_t)(k + q) * ldb));
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s8[q] = fmaf(vk[q], bk[q], s8[q]);
+    }
+    for (; k < rc; ++k) s8[0] = fmaf(__ldg(vv + k), bf16_bits_to_f32(__ldg(Bc + (size_t)k * ldb)), s8[0]);
   }
-  return s;
+  return ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
 }
 
 }  // namespace bdl

@@ -179,6 +179,14 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const bool whole = (kb0 == 0 && kb1 == p.k_blocks);
       const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
       float* my_part = p.part + ((size_t)(cta * 2 + slot) * BN) * kUmmaBM;
+      // LoRA expand term of the first 16 tokens, computed BEFORE waiting for the accumulator so its
+      // gathers overlap this tile's mainloop (v is ready: pdl_wait above).
+      float lr[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        lr[i] = 0.f;
+        if (i < tv && n < p.M) lr[i] = lora_expand_term(t0 + i, n, __ldg(p.ids + t0 + i), p.tab, p.arena, p.g, p.v, p.T);
+      }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
@@ -192,9 +200,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             for (int i = 0; i < 16; ++i) {
               const int t = t0 + c0 + i;
               if (c0 + i < tv) {
-                const int a = __ldg(p.ids + t);
-                const float y = __uint_as_float(r[i]) + lora_expand_term(t, n, a, p.tab, p.arena, p.g, p.v, p.T);
-                p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y);
+                const float lo = (c0 == 0) ? lr[i]
+                                           : lora_expand_term(t, n, __ldg(p.ids + t), p.tab, p.arena, p.g, p.v, p.T);
+                p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[i]) + lo);
               }
             }
           }
@@ -228,9 +236,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 const int sl = (ts > umma_u_lo(c, p.units, p.grid)) ? 1 : 0;
                 y += __ldcg(p.part + ((size_t)(c * 2 + sl) * BN + i) * kUmmaBM + row);
               }
-              const int a = __ldg(p.ids + t);
-              y += lora_expand_term(t, n, a, p.tab, p.arena, p.g, p.v, p.T);
-              p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y);
+              float lo = 0.f;
+#pragma unroll
+              for (int q2 = 0; q2 < 16; ++q2)
+                if (q2 == i) lo = lr[q2];
+              if (i >= 16) lo = lora_expand_term(t, n, __ldg(p.ids + t), p.tab, p.arena, p.g, p.v, p.T);
+              p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y + lo);
             }
           }
           if (etid == 0) p.tile_cnt[tile] = 0;
