@@ -108,4 +108,53 @@ __device__ __forceinline__ float lora_expand_term(int t, int n, int a, const Slo
   return ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
 }
 
+// LoRA expand term for up to 16 consecutive tokens tb..tb+cnt-1 at output column n (matmul_4/6):
+//   lr[i] = sum_c sum_k v[c][tb+i][j][k] * B_{a(tb+i),j}[c*re/C + k][n - e_lo_j]
+// Tokens are grouped by adapter (s_ids = their ids, shared memory) so each chunk of 16 rows of B is
+// gathered once per DISTINCT adapter with 16 independent loads in flight; consecutive threads hold
+// consecutive output columns, so every B row segment is read coalesced.
+__device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int cnt, const int* s_ids,
+                                             const SlotEntry* __restrict__ tab,
+                                             const __nv_bfloat16* __restrict__ arena, const Geom& g,
+                                             const float* __restrict__ v, int T) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) lr[i] = 0.f;
+  if (n >= g.M) return;
+  int j = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxSlices; ++q)
+    if (q < g.J && n >= g.col0[q]) j = q;
+  if (n < g.e_lo[j] || n >= g.e_hi[j]) return;
+  const int ldb = g.e_hi[j] - g.e_lo[j];
+  const int col = n - g.e_lo[j];
+  for (int i = 0; i < cnt; ++i) {
+    const int a = s_ids[i];
+    if (a < 0) continue;
+    bool seen = false;
+    for (int i2 = 0; i2 < i; ++i2) seen |= (s_ids[i2] == a);
+    if (seen) continue;
+    const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + tab[a].offB[j]) + col;
+    const int rc = tab[a].re / g.C;
+    for (int c = 0; c < g.C; ++c) {
+      for (int k0 = 0; k0 < rc; k0 += 16) {
+        float b[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          b[q] = (k0 + q < rc) ? bf16_bits_to_f32(__ldg(B + (size_t)(c * rc + k0 + q) * ldb)) : 0.f;
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          if (i2 >= i && i2 < cnt && s_ids[i2] == a) {
+            const float* vv = v + ((size_t)(c * T + tb + i2) * g.J + j) * g.Rc + k0;
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (k0 + q < rc) s = fmaf(__ldg(vv + q), b[q], s);
+            lr[i2] += s;
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace bdl

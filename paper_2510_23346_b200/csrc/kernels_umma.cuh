@@ -56,7 +56,7 @@ struct UmmaSmem {
   static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kBytes = kBarOff + 256 + 1024;  // + barriers/flags + alignment slack
+  static constexpr int kBytes = kBarOff + 256 + 1024 + 1024;  // + barriers/flags, ids, alignment slack
 };
 
 template <int BN>
@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
   int* s_last = (int*)(tmem_holder + 1);
+  int* s_ids = (int*)(smem + S::kBarOff + 256);  // [BN] adapter ids of the current token tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -168,6 +169,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     if (p.pdl) ptx::pdl_wait();         // v (shrink output) is complete and visible
     int acc = 0;
     uint32_t acc_phase = 0;
+    int cur_nt = -1;
     for (int u = u_lo; u < u_hi;) {
       const int tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks;
@@ -179,14 +181,16 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const bool whole = (kb0 == 0 && kb1 == p.k_blocks);
       const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
       float* my_part = p.part + ((size_t)(cta * 2 + slot) * BN) * kUmmaBM;
-      // LoRA expand term of the first 16 tokens, computed BEFORE waiting for the accumulator so its
-      // gathers overlap this tile's mainloop (v is ready: pdl_wait above).
-      float lr[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        lr[i] = 0.f;
-        if (i < tv && n < p.M) lr[i] = lora_expand_term(t0 + i, n, __ldg(p.ids + t0 + i), p.tab, p.arena, p.g, p.v, p.T);
+      if (nt != cur_nt) {  // stage this token tile's adapter ids
+        ptx::named_bar_sync(1, 128);
+        for (int i = etid; i < tv; i += 128) s_ids[i] = __ldg(p.ids + t0 + i);
+        ptx::named_bar_sync(1, 128);
+        cur_nt = nt;
       }
+      // LoRA term of the first 16 tokens, gathered BEFORE waiting for the accumulator so it overlaps
+      // this tile's mainloop.
+      float lr[16];
+      lora_chunk16(lr, n, t0, min(16, tv), s_ids, p.tab, p.arena, p.g, p.v, p.T);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
@@ -195,16 +199,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::tmem_ld_32x32b_x16(taddr + c0, r);
         ptx::tmem_ld_wait();
         if (whole) {
+          if (c0 > 0) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, p.tab, p.arena, p.g, p.v, p.T);
           if (n < p.M) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int t = t0 + c0 + i;
-              if (c0 + i < tv) {
-                const float lo = (c0 == 0) ? lr[i]
-                                           : lora_expand_term(t, n, __ldg(p.ids + t), p.tab, p.arena, p.g, p.v, p.T);
-                p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[i]) + lo);
-              }
-            }
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < tv) p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[i]) + lr[i]);
           }
         } else {
 #pragma unroll
@@ -228,20 +227,20 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           const int ts = tile * p.k_blocks;
           const int c_first = umma_cta_of(ts, p.units, p.grid);
           const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
-          if (n < p.M) {
-            for (int i = 0; i < tv; ++i) {
-              const int t = t0 + i;
-              float y = 0.f;
-              for (int c = c_first; c <= c_last; ++c) {
-                const int sl = (ts > umma_u_lo(c, p.units, p.grid)) ? 1 : 0;
-                y += __ldcg(p.part + ((size_t)(c * 2 + sl) * BN + i) * kUmmaBM + row);
-              }
-              float lo = 0.f;
+          for (int c0 = 0; c0 < tv; c0 += 16) {
+            if (c0 > 0 || tv > 16) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, p.tab, p.arena, p.g, p.v, p.T);
+            if (n < p.M) {
 #pragma unroll
-              for (int q2 = 0; q2 < 16; ++q2)
-                if (q2 == i) lo = lr[q2];
-              if (i >= 16) lo = lora_expand_term(t, n, __ldg(p.ids + t), p.tab, p.arena, p.g, p.v, p.T);
-              p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y + lo);
+              for (int i = 0; i < 16; ++i) {
+                if (c0 + i < tv) {
+                  float y = 0.f;
+                  for (int c = c_first; c <= c_last; ++c) {
+                    const int sl = (ts > umma_u_lo(c, p.units, p.grid)) ? 1 : 0;
+                    y += __ldcg(p.part + ((size_t)(c * 2 + sl) * BN + c0 + i) * kUmmaBM + row);
+                  }
+                  p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(y + lr[i]);
+                }
+              }
             }
           }
           if (etid == 0) p.tile_cnt[tile] = 0;
