@@ -37,7 +37,7 @@ struct UmmaParams {
   Geom g;
   const float* v;
   __nv_bfloat16* Y;
-  float* part;    // [grid][2][BN][128]
+  float* part;    // [grid + 1][128][BN] fp32 split-tile accumulators, zero between launches
   int* tile_cnt;  // [m_tiles * n_tiles], zero between launches
   int pdl;
 };
@@ -179,8 +179,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const int t0 = nt * BN;
       const int tv = min(BN, p.T - t0);
       const bool whole = (kb0 == 0 && kb1 == p.k_blocks);
-      const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
-      float* my_part = p.part + ((size_t)(cta * 2 + slot) * BN) * kUmmaBM;
+      // a split tile accumulates in the slot of the first CTA boundary inside it (unique per tile)
+      const int bslot = umma_cta_of((long long)tile * p.k_blocks, p.units, p.grid) + 1;
+      float* my_acc = p.part + ((size_t)bslot * kUmmaBM + row) * BN;
       if (nt != cur_nt) {  // stage this token tile's adapter ids
         ptx::named_bar_sync(1, 128);
         for (int i = etid; i < tv; i += 128) s_ids[i] = __ldg(p.ids + t0 + i);
@@ -206,17 +207,20 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               if (c0 + i < tv) p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[i]) + lr[i]);
           }
         } else {
+          // split tile: fp32 vector reduction into the tile's boundary slot (columns >= tv hold exact
+          // zeros -- TMA zero-fills out-of-range token rows -- so whole 16-column chunks are added)
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c0 + i < tv) my_part[(size_t)(c0 + i) * kUmmaBM + row] = __uint_as_float(r[i]);
+          for (int i = 0; i < 16; i += 4)
+            ptx::red_add_v4(my_acc + c0 + i, __uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                            __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
       if (!whole) {
+        __threadfence();  // this thread's reductions before the arrival count
         ptx::named_bar_sync(1, 128);
         if (etid == 0) {
-          __threadfence();
           const int got = kb1 - kb0;
           const int old = atomicAdd(p.tile_cnt + tile, got);
           *s_last = (old + got == p.k_blocks);
@@ -224,23 +228,22 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::named_bar_sync(1, 128);
         if (*s_last) {
           __threadfence();
-          const int ts = tile * p.k_blocks;
-          const int c_first = umma_cta_of(ts, p.units, p.grid);
-          const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
           for (int c0 = 0; c0 < tv; c0 += 16) {
             if (c0 > 0 || tv > 16) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, p.tab, p.arena, p.g, p.v, p.T);
+            float y[16];
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+              const float4 a4 = __ldcg(reinterpret_cast<const float4*>(my_acc + c0 + i));
+              y[i] = a4.x;
+              y[i + 1] = a4.y;
+              y[i + 2] = a4.z;
+              y[i + 3] = a4.w;
+              __stcg(reinterpret_cast<float4*>(my_acc + c0 + i), make_float4(0.f, 0.f, 0.f, 0.f));  // re-arm
+            }
             if (n < p.M) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                if (c0 + i < tv) {
-                  float y = 0.f;
-                  for (int c = c_first; c <= c_last; ++c) {
-                    const int sl = (ts > umma_u_lo(c, p.units, p.grid)) ? 1 : 0;
-                    y += __ldcg(p.part + ((size_t)(c * 2 + sl) * BN + c0 + i) * kUmmaBM + row);
-                  }
-                  p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(y + lr[i]);
-                }
-              }
+              for (int i = 0; i < 16; ++i)
+                if (c0 + i < tv) p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(y[i] + lr[i]);
             }
           }
           if (etid == 0) p.tile_cnt[tile] = 0;
@@ -267,7 +270,7 @@ inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
   const int BN = umma_bn_for(T);
   const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM;
   const int n_tiles = (T + BN - 1) / BN;
-  size_t part = (size_t)num_sms * 2 * BN * kUmmaBM * sizeof(float);
+  size_t part = (size_t)(num_sms + 1) * BN * kUmmaBM * sizeof(float);
   size_t cnt = (size_t)m_tiles * n_tiles * sizeof(int);
   return ((cnt + 255) / 256) * 256 + part;
 }
