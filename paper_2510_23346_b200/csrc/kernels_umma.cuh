@@ -37,7 +37,7 @@ struct UmmaParams {
   Geom g;
   const float* v;
   __nv_bfloat16* Y;
-  float* part;    // [grid + 1][128][BN] fp32 split-tile accumulators, zero between launches
+  float* part;    // [grid][2][128][BN] fp32 split-tile partials (slot 0: a CTA's first segment, 1: last)
   int* tile_cnt;  // [m_tiles * n_tiles], zero between launches
   int pdl;
 };
@@ -179,9 +179,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const int t0 = nt * BN;
       const int tv = min(BN, p.T - t0);
       const bool whole = (kb0 == 0 && kb1 == p.k_blocks);
-      // a split tile accumulates in the slot of the first CTA boundary inside it (unique per tile)
-      const int bslot = umma_cta_of((long long)tile * p.k_blocks, p.units, p.grid) + 1;
-      float* my_acc = p.part + ((size_t)bslot * kUmmaBM + row) * BN;
+      const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
+      float* my_part = p.part + ((size_t)(cta * 2 + slot) * kUmmaBM + row) * BN;
       if (nt != cur_nt) {  // stage this token tile's adapter ids
         ptx::named_bar_sync(1, 128);
         for (int i = etid; i < tv; i += 128) s_ids[i] = __ldg(p.ids + t0 + i);
@@ -207,18 +206,19 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               if (c0 + i < tv) p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[i]) + lr[i]);
           }
         } else {
-          // split tile: fp32 vector reduction into the tile's boundary slot (columns >= tv hold exact
-          // zeros -- TMA zero-fills out-of-range token rows -- so whole 16-column chunks are added)
+          // split tile: this CTA's fp32 partial, [row][BN] in its own slot (0 = its first segment,
+          // 1 = its last).  Columns >= tv hold exact zeros (TMA zero-fills out-of-range tokens).
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
-            ptx::red_add_v4(my_acc + c0 + i, __uint_as_float(r[i]), __uint_as_float(r[i + 1]),
-                            __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+            __stcg(reinterpret_cast<float4*>(my_part + c0 + i),
+                   make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+                               __uint_as_float(r[i + 3])));
         }
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
       if (!whole) {
-        __threadfence();  // this thread's reductions before the arrival count
+        __threadfence();  // this thread's partial before the arrival count
         ptx::named_bar_sync(1, 128);
         if (etid == 0) {
           const int got = kb1 - kb0;
@@ -227,18 +227,39 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         }
         ptx::named_bar_sync(1, 128);
         if (*s_last) {
+          // finisher: sum the contributors' partials in CTA order (deterministic), 8 contributors'
+          // loads in flight per round, add the LoRA term, round once, store.
           __threadfence();
+          const int ts = tile * p.k_blocks;
+          const int c_first = umma_cta_of(ts, p.units, p.grid);
+          const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
           for (int c0 = 0; c0 < tv; c0 += 16) {
             if (c0 > 0 || tv > 16) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, p.tab, p.arena, p.g, p.v, p.T);
+            const int nq = min(4, (tv - c0 + 3) / 4);  // float4 groups holding valid tokens
             float y[16];
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              const float4 a4 = __ldcg(reinterpret_cast<const float4*>(my_acc + c0 + i));
-              y[i] = a4.x;
-              y[i + 1] = a4.y;
-              y[i + 2] = a4.z;
-              y[i + 3] = a4.w;
-              __stcg(reinterpret_cast<float4*>(my_acc + c0 + i), make_float4(0.f, 0.f, 0.f, 0.f));  // re-arm
+            for (int i = 0; i < 16; ++i) y[i] = 0.f;
+            for (int cb = c_first; cb <= c_last; cb += 8) {
+              float4 buf[8][4];
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc) {
+                const int c = cb + cc;
+                const int sl = (c <= c_last && ts > umma_u_lo(c, p.units, p.grid)) ? 1 : 0;
+                const float4* src = reinterpret_cast<const float4*>(
+                    p.part + ((size_t)(min(c, c_last) * 2 + sl) * kUmmaBM + row) * BN + c0);
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4)
+                  buf[cc][g4] = (c <= c_last && g4 < nq) ? __ldcg(src + g4) : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc)
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) {
+                  y[4 * g4] += buf[cc][g4].x;
+                  y[4 * g4 + 1] += buf[cc][g4].y;
+                  y[4 * g4 + 2] += buf[cc][g4].z;
+                  y[4 * g4 + 3] += buf[cc][g4].w;
+                }
             }
             if (n < p.M) {
 #pragma unroll
@@ -270,7 +291,7 @@ inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
   const int BN = umma_bn_for(T);
   const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM;
   const int n_tiles = (T + BN - 1) / BN;
-  size_t part = (size_t)(num_sms + 1) * BN * kUmmaBM * sizeof(float);
+  size_t part = (size_t)num_sms * 2 * BN * kUmmaBM * sizeof(float);
   size_t cnt = (size_t)m_tiles * n_tiles * sizeof(int);
   return ((cnt + 255) / 256) * 256 + part;
 }
@@ -350,7 +371,8 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   const long long units = (long long)p.m_tiles * p.n_tiles * p.k_blocks;
   if (units > (1LL << 30)) return 1;
   p.units = (int)units;
-  p.grid = (int)std::min<long long>(units, num_sms);
+  // >= 8 k-blocks per CTA: bounds the contributors of a split tile (finisher latency) on small shapes
+  p.grid = (int)std::max<long long>(1, std::min<long long>(units / 8, num_sms));
   p.ids = ids;
   p.tab = tab;
   p.arena = arena;
