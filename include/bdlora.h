@@ -94,6 +94,9 @@ int bdlora_device_check(int cuda_device);
 /* Number of kernels this library has enqueued since it was loaded (host-side count of launches;
    a CUDA-graph replay re-runs the captured launches without counting them again).              */
 int bdlora_kernel_launches(int64_t* n);
+/* Profiling hook: if non-NULL, subsequent tensor-core GEMM launches record per-CTA %globaltimer
+   stamps (16 int64 per CTA) into this device buffer (>= 148*16*8 bytes); NULL turns it off.      */
+int bdlora_debug_trace(void* device_buffer);
 
 /* ---------------------------------------------------------------- communicator (NCCL) ------- */
 /* NCCL 2.28 over NVLink/NVSwitch.  Bootstrap: rank 0 calls bdlora_comm_unique_id, the caller

@@ -324,3 +324,8 @@ def bdlora_base_expand(pool: Pool, X, W, ids, v, Y, ws, stream=None) -> None:
     _need(v, "v", dtype=torch.float32, device=pool.tdevice)
     call("bdlora_base_expand", pool.handle, _ptr(X), T, _ptr(W), _ptr(ids), _ptr(v), _ptr(Y), _ptr(ws), ws.numel(),
          _stream(stream))
+
+
+def bdlora_debug_trace(buf) -> None:
+    """Profiling hook: per-CTA timestamps of subsequent GEMM launches into `buf` (device int64), or None."""
+    call("bdlora_debug_trace", None if buf is None else buf.data_ptr())

@@ -40,7 +40,18 @@ struct UmmaParams {
   float* part;    // [grid][2][128][BN] fp32 split-tile partials (slot 0: a CTA's first segment, 1: last)
   int* tile_cnt;  // [m_tiles * n_tiles], zero between launches
   int pdl;
+  long long* trace;  // optional per-CTA timestamps (ns, %globaltimer) for profiling; nullptr = off
 };
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define UMMA_TRACE(slot)                                              \
+  do {                                                                \
+    if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = gtimer(); \
+  } while (0)
 
 __device__ __forceinline__ int umma_u_lo(long long c, int units, int grid) { return (int)(c * units / grid); }
 __device__ __forceinline__ int umma_cta_of(long long u, int units, int grid) {
@@ -80,6 +91,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   const int cta = blockIdx.x;
   const int u_lo = umma_u_lo(cta, p.units, p.grid);
   const int u_hi = umma_u_lo(cta + 1, p.units, p.grid);
+  if (threadIdx.x == 0) UMMA_TRACE(0);
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmW);
@@ -100,6 +112,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) UMMA_TRACE(1);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -118,6 +131,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
           ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
           ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
+          if (u == u_lo && kb == kb0) UMMA_TRACE(2);
           if (++stage == S::kStages) {
             stage = 0;
             phase ^= 1;
@@ -144,6 +158,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (u == u_lo && kb == kb0) UMMA_TRACE(3);
           const uint64_t a_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sW + stage * S::kWBytes));
           const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sX + stage * S::kXBytes));
 #pragma unroll
@@ -156,6 +171,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           }
         }
         ptx::mma_commit(&tfull[acc]);
+        UMMA_TRACE(4);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         u += kb1 - kb0;
@@ -193,6 +209,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       lora_chunk16(lr, n, t0, min(16, tv), s_ids, p.tab, p.arena, p.g, p.v, p.T);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
+      if (etid == 0) {
+        if (u == u_lo) UMMA_TRACE(5);
+        UMMA_TRACE(6);
+      }
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       for (int c0 = 0; c0 < tv; c0 += 16) {
         uint32_t r[16];
@@ -274,17 +294,21 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       u += kb1 - kb0;
+      if (etid == 0) UMMA_TRACE(7);
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  if (threadIdx.x == 0) UMMA_TRACE(8);
   if (warp == 1) ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
 }
 
 // ------------------------------------------------------------------------------------------------
 // Host side
 // ------------------------------------------------------------------------------------------------
+inline long long* g_umma_trace = nullptr;  // profiling hook (bdlora_debug_trace)
+
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
 
 inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
@@ -383,6 +407,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.tile_cnt = (int*)ws;
   p.part = (float*)((char*)ws + cnt_bytes);
   p.pdl = pdl;
+  p.trace = g_umma_trace;
   switch (BN) {
     case 16: return umma_launch_bn<16>(p, X, W, st);
     case 32: return umma_launch_bn<32>(p, X, W, st);

@@ -280,6 +280,11 @@ extern "C" {
 
 int bdlora_abi_version(void) { return BDLORA_ABI_VERSION; }
 
+int bdlora_debug_trace(void* device_buffer) {
+  bdl::g_umma_trace = (long long*)device_buffer;
+  return BDLORA_OK;
+}
+
 int bdlora_kernel_launches(int64_t* n) {
   if (!n) return fail(BDLORA_E_ARG, "n is NULL");
   *n = g_launches.load();
