@@ -110,11 +110,13 @@ __device__ __forceinline__ float lora_expand_term(int t, int n, int a, const Slo
 
 // LoRA expand term for up to 16 consecutive tokens tb..tb+cnt-1 at output column n (matmul_4/6):
 //   lr[i] = sum_c sum_k v[c][tb+i][j][k] * B_{a(tb+i),j}[c*re/C + k][n - e_lo_j]
-// Tokens are grouped by adapter (s_ids = their ids, shared memory) so each chunk of 16 rows of B is
-// gathered once per DISTINCT adapter with 16 independent loads in flight; consecutive threads hold
-// consecutive output columns, so every B row segment is read coalesced.
+// Tokens are grouped by adapter (s_lead[i] = index in [0,16) of the first token of this chunk with the
+// same id, -1 for id -1; staged in shared memory) so each 16-row chunk of B is gathered once per
+// DISTINCT adapter, 16 independent loads in flight; consecutive threads hold consecutive output
+// columns, so every B row segment is read coalesced.  v values are loaded before use and reduced in
+// 4 independent chains (no load->FMA latency chain).
 __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int cnt, const int* s_ids,
-                                             const SlotEntry* __restrict__ tab,
+                                             const int* s_lead, const SlotEntry* __restrict__ tab,
                                              const __nv_bfloat16* __restrict__ arena, const Geom& g,
                                              const float* __restrict__ v, int T) {
 #pragma unroll
@@ -128,11 +130,8 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
   const int ldb = g.e_hi[j] - g.e_lo[j];
   const int col = n - g.e_lo[j];
   for (int i = 0; i < cnt; ++i) {
+    if (s_lead[i] != i) continue;  // not a group leader (or no adapter)
     const int a = s_ids[i];
-    if (a < 0) continue;
-    bool seen = false;
-    for (int i2 = 0; i2 < i; ++i2) seen |= (s_ids[i2] == a);
-    if (seen) continue;
     const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + tab[a].offB[j]) + col;
     const int rc = tab[a].re / g.C;
     for (int c = 0; c < g.C; ++c) {
@@ -143,13 +142,20 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
           b[q] = (k0 + q < rc) ? bf16_bits_to_f32(__ldg(B + (size_t)(c * rc + k0 + q) * ldb)) : 0.f;
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
-          if (i2 >= i && i2 < cnt && s_ids[i2] == a) {
+          if (i2 < cnt && s_lead[i2] == i) {
             const float* vv = v + ((size_t)(c * T + tb + i2) * g.J + j) * g.Rc + k0;
-            float s = 0.f;
+            float vk[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              if (k0 + q < rc) s = fmaf(__ldg(vv + q), b[q], s);
-            lr[i2] += s;
+            for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? __ldg(vv + q) : 0.f;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+              s0 = fmaf(vk[q], b[q], s0);
+              s1 = fmaf(vk[q + 1], b[q + 1], s1);
+              s2 = fmaf(vk[q + 2], b[q + 2], s2);
+              s3 = fmaf(vk[q + 3], b[q + 3], s3);
+            }
+            lr[i2] += (s0 + s1) + (s2 + s3);
           }
         }
       }

@@ -67,7 +67,7 @@ struct UmmaSmem {
   static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kBytes = kBarOff + 256 + 1024 + 1024;  // + barriers/flags, ids, alignment slack
+  static constexpr int kBytes = kBarOff + 256 + 2048 + 1024;  // + barriers/flags, ids/leaders, alignment slack
 };
 
 template <int BN>
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
   int* s_last = (int*)(tmem_holder + 1);
   int* s_ids = (int*)(smem + S::kBarOff + 256);  // [BN] adapter ids of the current token tile
+  int* s_lead = s_ids + 256;                     // [BN] group leader of each token in its 16-chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -201,12 +202,26 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::named_bar_sync(1, 128);
         for (int i = etid; i < tv; i += 128) s_ids[i] = __ldg(p.ids + t0 + i);
         ptx::named_bar_sync(1, 128);
+        for (int i = etid; i < tv; i += 128) {  // group leader within the token's 16-chunk
+          const int cb = i & ~15, a = s_ids[i];
+          int lead = -1;
+          if (a >= 0) {
+            lead = i - cb;
+            for (int i2 = cb; i2 < i; ++i2)
+              if (s_ids[i2] == a) {
+                lead = i2 - cb;
+                break;
+              }
+          }
+          s_lead[i] = lead;
+        }
+        ptx::named_bar_sync(1, 128);
         cur_nt = nt;
       }
       // LoRA term of the first 16 tokens, gathered BEFORE waiting for the accumulator so it overlaps
       // this tile's mainloop.
       float lr[16];
-      lora_chunk16(lr, n, t0, min(16, tv), s_ids, p.tab, p.arena, p.g, p.v, p.T);
+      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       if (etid == 0) {
@@ -219,7 +234,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::tmem_ld_32x32b_x16(taddr + c0, r);
         ptx::tmem_ld_wait();
         if (whole) {
-          if (c0 > 0) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, p.tab, p.arena, p.g, p.v, p.T);
+          if (c0 > 0) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T);
           if (n < p.M) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -238,23 +253,23 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
       if (!whole) {
-        __threadfence();  // this thread's partial before the arrival count
+        // arrival: CTA barrier, then ONE thread publishes with a gpu-scope acq_rel atomic (the
+        // barrier + cumulative fence order every thread's partial before it)
         ptx::named_bar_sync(1, 128);
         if (etid == 0) {
           const int got = kb1 - kb0;
-          const int old = atomicAdd(p.tile_cnt + tile, got);
+          const int old = ptx::atom_add_acq_rel_gpu(p.tile_cnt + tile, got);
           *s_last = (old + got == p.k_blocks);
         }
         ptx::named_bar_sync(1, 128);
         if (*s_last) {
           // finisher: sum the contributors' partials in CTA order (deterministic), 8 contributors'
           // loads in flight per round, add the LoRA term, round once, store.
-          __threadfence();
           const int ts = tile * p.k_blocks;
           const int c_first = umma_cta_of(ts, p.units, p.grid);
           const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
           for (int c0 = 0; c0 < tv; c0 += 16) {
-            if (c0 > 0 || tv > 16) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, p.tab, p.arena, p.g, p.v, p.T);
+            if (c0 > 0 || tv > 16) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T);
             const int nq = min(4, (tv - c0 + 3) / 4);  // float4 groups holding valid tokens
             float y[16];
 #pragma unroll
