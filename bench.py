@@ -245,42 +245,23 @@ def algorithmic(wl, sharding, n, ids_np):
 
 # ============================================================================ timing
 
-def time_layer(bd, torch, layer, comm, ids, steps, warmup, use_graph, barrier):
-    """Returns (total_ms, per_projection_ms_lists, launches_per_step)."""
-    dev = layer[0].X.device
-    s = torch.cuda.current_stream(dev)
-    l0 = bd.bdlora_kernel_launches()
-    for p in layer:
-        p.run(bd, comm, ids, 0)
-    launches = bd.bdlora_kernel_launches() - l0
-    for w in range(max(0, warmup - 1)):
-        for p in layer:
-            p.run(bd, comm, ids, w + 1)
-    torch.cuda.synchronize()
-    nproj = len(layer)
-    evs = [[torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(nproj + 1)] for _ in range(steps)]
-
-    def body():
-        for k in range(steps):
-            evs[k][0].record()
-            for j, p in enumerate(layer):
-                p.run(bd, comm, ids, k)
-                evs[k][j + 1].record()
-
+def graph_time(torch, body, steps, barrier, use_graph=True):
+    """Capture `steps` calls of body(k) in ONE CUDA graph, replay once (warm), then time one replay with
+    CUDA events on the launching stream, bracketed by barrier + synchronize.  Returns total ms."""
     g = None
     if use_graph:
-        g = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(dev)
+        s = torch.cuda.current_stream()
+        side = torch.cuda.Stream()
         side.wait_stream(s)
         with torch.cuda.stream(side):
-            # warm the capture stream once (allocator / lazy init), then capture
-            for p in layer:
-                p.run(bd, comm, ids, 0)
+            body(0)  # warm the capture stream
         s.wait_stream(side)
         torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            body()
-        g.replay()  # warm replay (untimed)
+            for k in range(steps):
+                body(k)
+        g.replay()
         torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
@@ -290,15 +271,36 @@ def time_layer(bd, torch, layer, comm, ids, steps, warmup, use_graph, barrier):
     if g is not None:
         g.replay()
     else:
-        body()
+        for k in range(steps):
+            body(k)
     end.record()
     torch.cuda.synchronize()
     barrier()
-    total = start.elapsed_time(end)
-    per = [[evs[k][j].elapsed_time(evs[k][j + 1]) for k in range(steps)] for j in range(nproj)]
+    return start.elapsed_time(end)
+
+
+def time_layer(bd, torch, layer, comm, ids, steps, warmup, use_graph, barrier):
+    """Returns (total_ms of `steps` layer steps, per-projection isolated us, launches per step)."""
+    l0 = bd.bdlora_kernel_launches()
+    for p in layer:
+        p.run(bd, comm, ids, 0)
+    launches = bd.bdlora_kernel_launches() - l0
+    for w in range(max(0, warmup - 1)):
+        for p in layer:
+            p.run(bd, comm, ids, w + 1)
+    torch.cuda.synchronize()
+
+    def step(k):
+        for p in layer:
+            p.run(bd, comm, ids, k)
+
+    total = graph_time(torch, step, steps, barrier, use_graph)
+    # each projection alone, same launch configuration, weights rotated like in the step
+    per = []
+    for p in layer:
+        ms = graph_time(torch, lambda k, p=p: p.run(bd, comm, ids, k), steps, barrier, use_graph)
+        per.append(ms / steps * 1e3)
     return total, per, launches
-
-
 def time_e2e(bd, torch, layer, comm, ids_np, steps, warmup, barrier):
     """Same step through the public API with HOST buffers: pinned H2D of every projection's input and
     the ids, the four forwards, D2H of every output -- all inside the timed region (graph-captured)."""
@@ -463,12 +465,12 @@ def run_ours(args, wl):
     ms_step = total_ms / args.steps
     value = T / (ms_step * 1e-3)
     names = [p.proj.name for p in layer]
-    proj_us = {nm: statistics.median(x) * 1e3 for nm, x in zip(names, per)}
+    proj_us = dict(zip(names, per))
     alg = algorithmic(wl, "bd", n, ids_np)
 
     # dominant kernel = the base GEMM + fused expand of the projection with the most time
     dom = max(names, key=lambda nm: proj_us[nm])
-    dom_mean_us = statistics.mean(per[names.index(dom)]) * 1e3
+    dom_mean_us = per[names.index(dom)]
     dom_bytes, dom_flops = alg[dom]
     bound = "hbm" if dom_flops / dom_bytes < (tf_peak * 1e12) / (hbm_peak * 1e9) else "tensor"
     if bound == "hbm":
@@ -507,7 +509,7 @@ def run_ours(args, wl):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             s_total = float(t.item())
         slora = {"ms_per_step": s_total / args.steps, "tokens_per_s": T / (s_total / args.steps * 1e-3),
-                 "proj_us": {nm: statistics.median(x) * 1e3 for nm, x in zip(names, s_per)},
+                 "proj_us": dict(zip(names, s_per)),
                  "bd_speedup": (s_total / total_ms)}
         if comm is not None:
             slora["collectives"] = bd.bdlora_comm_stats(comm)
@@ -587,43 +589,28 @@ def time_layer_local(bd, torch, layer, ids, steps, warmup, tpn):
 
     def run(p, k):
         W = p.W[k % len(p.W)]
-        ids_ = ids
         if p.sharding == "bd":
             if p.proj.parallel == "column":
-                bd.bdlora_column_forward(p.pool, p.X, W, ids_, p.Y, p.ws)
+                bd.bdlora_column_forward(p.pool, p.X, W, ids, p.Y, p.ws)
             else:
-                bd.bdlora_row_partial(p.pool, p.X, W, ids_, p.Y, p.ws)
+                bd.bdlora_row_partial(p.pool, p.X, W, ids, p.Y, p.ws)
         else:
             if id(p) not in vbufs:
                 T = p.X.shape[0]
                 c = tpn if p.proj.parallel == "column" else 1
                 vbufs[id(p)] = torch.zeros(c * bd.bdlora_v_elems(p.pool, T), dtype=torch.float32, device=dev)
             v = vbufs[id(p)]
-            bd.bdlora_lora_shrink(p.pool, p.X, ids_, v, p.ws)
-            bd.bdlora_base_expand(p.pool, p.X, W, ids_, v, p.Y, p.ws)
+            bd.bdlora_lora_shrink(p.pool, p.X, ids, v, p.ws)
+            bd.bdlora_base_expand(p.pool, p.X, W, ids, v, p.Y, p.ws)
 
     for w in range(warmup):
         for p in layer:
             run(p, w)
     torch.cuda.synchronize()
-    nproj = len(layer)
-    evs = [[torch.cuda.Event(enable_timing=True, external=True) for _ in range(nproj + 1)] for _ in range(steps)]
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        for k in range(steps):
-            evs[k][0].record()
-            for j, p in enumerate(layer):
-                run(p, k)
-                evs[k][j + 1].record()
-    g.replay()
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    g.replay()
-    e.record()
-    torch.cuda.synchronize()
-    per = [statistics.median([evs[k][j].elapsed_time(evs[k][j + 1]) for k in range(steps)]) * 1e3 for j in range(nproj)]
-    return s.elapsed_time(e) / steps, per, None
+    nobar = lambda: None  # noqa: E731
+    total = graph_time(torch, lambda k: [run(p, k) for p in layer], steps, nobar)
+    per = [graph_time(torch, lambda k, p=p: run(p, k), steps, nobar) / steps * 1e3 for p in layer]
+    return total / steps, per, None
 
 
 def main():

@@ -94,6 +94,13 @@ int bdlora_device_check(int cuda_device);
 /* Number of kernels this library has enqueued since it was loaded (host-side count of launches;
    a CUDA-graph replay re-runs the captured launches without counting them again).              */
 int bdlora_kernel_launches(int64_t* n);
+/* Programmatic dependent launch chaining (default ON): every kernel of a forward is launched with
+   programmatic stream serialization and waits (griddepcontrol.wait) before reading anything the
+   preceding kernel may have produced (X, ids, v) and before writing Y, so a forward's prologue and
+   weight stream overlap the tail of the preceding kernel.  Contract while ON: the base weight W and
+   the pool's adapter factors must not be written by the kernel immediately preceding a forward on
+   the same stream (they are streamed before the dependency resolves).  0 = plain stream order.   */
+int bdlora_set_pdl(int enable);
 /* Profiling hook: if non-NULL, subsequent tensor-core GEMM launches record per-CTA %globaltimer
    stamps (16 int64 per CTA) into this device buffer (>= 148*16*8 bytes); NULL turns it off.      */
 int bdlora_debug_trace(void* device_buffer);

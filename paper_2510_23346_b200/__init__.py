@@ -329,3 +329,8 @@ def bdlora_base_expand(pool: Pool, X, W, ids, v, Y, ws, stream=None) -> None:
 def bdlora_debug_trace(buf) -> None:
     """Profiling hook: per-CTA timestamps of subsequent GEMM launches into `buf` (device int64), or None."""
     call("bdlora_debug_trace", None if buf is None else buf.data_ptr())
+
+
+def bdlora_set_pdl(enable: bool) -> None:
+    """Programmatic-dependent-launch chaining of the library's kernels (default on; see bdlora.h)."""
+    call("bdlora_set_pdl", 1 if enable else 0)

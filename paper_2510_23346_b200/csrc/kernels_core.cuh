@@ -149,6 +149,8 @@ __global__ void __launch_bounds__(128) shrink_rows_kernel(const __nv_bfloat16* _
                                                           const __nv_bfloat16* __restrict__ arena, Geom g,
                                                           float* __restrict__ v) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // programmatic dependency: X and ids may be produced by the preceding kernel
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ int s_members[];  // [T]
   __shared__ int s_cnt, s_dup;
   __shared__ float s_red[4][MT];

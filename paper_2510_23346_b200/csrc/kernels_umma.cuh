@@ -113,32 +113,46 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  if (threadIdx.x == 0) UMMA_TRACE(1);
+  if (threadIdx.x == 0) {
+    UMMA_TRACE(1);
+    // dependents (the next kernel) may launch now: they wait for this grid's completion before
+    // touching anything it writes, and can only take SMs this grid has released.
+    ptx::pdl_launch_dependents();
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
+    // Weights never depend on the preceding kernel: the first ring of W tiles is issued BEFORE the
+    // programmatic-dependency wait (overlapping the previous kernel's tail), activations after it.
     if (ptx::elect_one()) {
       const uint64_t pol_w = ptx::policy_evict_first();
       const uint64_t pol_x = ptx::policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = u_lo; u < u_hi;) {
-        const int tile = u / p.k_blocks;
-        const int kb0 = u - tile * p.k_blocks;
-        const int kb1 = min(p.k_blocks, kb0 + (u_hi - u));
+      const int nu = u_hi - u_lo;
+      const int P = min(nu, S::kStages);
+      for (int idx = 0; idx < P; ++idx) {
+        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, mt = tile % p.m_tiles;
+        ptx::mbar_arrive_expect_tx(&full[idx], S::kStageBytes);
+        ptx::tma_load_2d(sW + idx * S::kWBytes, &tmW, &full[idx], kb * kUmmaBK, mt * kUmmaBM, pol_w);
+      }
+      if (nu > 0) UMMA_TRACE(2);
+      if (p.pdl) ptx::pdl_wait();
+      for (int idx = 0; idx < P; ++idx) {
+        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, nt = tile / p.m_tiles;
+        ptx::tma_load_2d(sX + idx * S::kXBytes, &tmX, &full[idx], kb * kUmmaBK, nt * BN, pol_x);
+      }
+      int stage = (P == S::kStages) ? 0 : P;
+      uint32_t phase = (P == S::kStages) ? 1u : 0u;
+      for (int idx = P; idx < nu; ++idx) {
+        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks;
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
-          ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
-          ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
-          if (u == u_lo && kb == kb0) UMMA_TRACE(2);
-          if (++stage == S::kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+        ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
+        ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
+        if (++stage == S::kStages) {
+          stage = 0;
+          phase ^= 1;
         }
-        u += kb1 - kb0;
       }
     }
   } else if (warp == 1) {
@@ -183,7 +197,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..127
-    if (p.pdl) ptx::pdl_wait();         // v (shrink output) is complete and visible
+    if (p.pdl) ptx::pdl_wait();         // the preceding kernel (shrink: v) is complete and visible;
+                                        // also orders our Y writes after every earlier reader
     int acc = 0;
     uint32_t acc_phase = 0;
     int cur_nt = -1;
@@ -253,6 +268,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
       if (!whole) {
+        if (etid == 0) UMMA_TRACE(12);
         // arrival: CTA barrier, then ONE thread publishes with a gpu-scope acq_rel atomic (the
         // barrier + cumulative fence order every thread's partial before it)
         ptx::named_bar_sync(1, 128);
@@ -262,9 +278,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           *s_last = (old + got == p.k_blocks);
         }
         ptx::named_bar_sync(1, 128);
+        if (etid == 0) UMMA_TRACE(11);
         if (*s_last) {
           // finisher: sum the contributors' partials in CTA order (deterministic), 8 contributors'
           // loads in flight per round, add the LoRA term, round once, store.
+          if (etid == 0) UMMA_TRACE(9);
           const int ts = tile * p.k_blocks;
           const int c_first = umma_cta_of(ts, p.units, p.grid);
           const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
@@ -302,7 +320,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 if (c0 + i < tv) p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(y[i] + lr[i]);
             }
           }
-          if (etid == 0) p.tile_cnt[tile] = 0;
+          if (etid == 0) {
+            p.tile_cnt[tile] = 0;
+            UMMA_TRACE(10);
+          }
         }
         ptx::named_bar_sync(1, 128);  // s_last reused by the next segment
       }

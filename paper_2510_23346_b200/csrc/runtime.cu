@@ -182,16 +182,25 @@ int check_fwd_args(const bdlora_pool* p, const void* X, int64_t T, const void* W
 }
 
 // ---------------------------------------------------------------------------- launches
+int g_pdl = 1;  // programmatic dependent launch chaining (bdlora_set_pdl)
+
 int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids, float* v, cudaStream_t st) {
   if (T == 0) return BDLORA_OK;
   const Geom& g = p->g;
   if (T > 65535 * 16) return fail(BDLORA_E_CAPACITY, "T = %d too large for the shrink grid", T);
-  dim3 grid(T, g.J, p->rs_max);
-  const size_t smem = sizeof(int) * (size_t)T;
-  bdl::shrink_rows_kernel<4><<<grid, 128, smem, st>>>((const __nv_bfloat16*)X, T, ids, p->d_tab,
-                                                      (const __nv_bfloat16*)p->arena, g, v);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(T, g.J, p->rs_max);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = sizeof(int) * (size_t)T;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CU_TRY(cudaLaunchKernelEx(&cfg, bdl::shrink_rows_kernel<4>, (const __nv_bfloat16*)X, T, ids,
+                            (const SlotEntry*)p->d_tab, (const __nv_bfloat16*)p->arena, g, v));
   count_launch();
-  CU_TRY(cudaGetLastError());
   return BDLORA_OK;
 }
 
@@ -236,7 +245,8 @@ int launch_gemv(const bdlora_pool* p, const void* X, int T, const void* W, const
 }
 
 int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W, const int32_t* ids, const float* v,
-                       void* Y, void* ws, cudaStream_t st, int pdl = 0) {
+                       void* Y, void* ws, cudaStream_t st) {
+  const int pdl = g_pdl;
   if (T == 0) return BDLORA_OK;
   if (bdl::umma_eligible(p->g, T)) {
     const WsLayout L = ws_layout(p, T);
@@ -279,6 +289,11 @@ int require_comm(const bdlora_pool* p, const bdlora_comm* c, const char* fn) {
 extern "C" {
 
 int bdlora_abi_version(void) { return BDLORA_ABI_VERSION; }
+
+int bdlora_set_pdl(int enable) {
+  g_pdl = enable ? 1 : 0;
+  return BDLORA_OK;
+}
 
 int bdlora_debug_trace(void* device_buffer) {
   bdl::g_umma_trace = (long long*)device_buffer;
@@ -724,7 +739,7 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
   float* v = ws_v(p, ws, T);
   ST_TRY(launch_shrink(p, X, (int)T, ids, v, st));
   // programmatic dependent launch: the GEMM streams W while the shrink runs; only its epilogue waits
-  return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st, /*pdl=*/1);
+  return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st);
 }
 
 int bdlora_column_forward(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y,

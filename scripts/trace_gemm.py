@@ -39,8 +39,13 @@ t = tr.view(148, 16).cpu().numpy().astype("int64")
 used = t[:, 0] > 0
 t = t[used]
 t0 = t[:, 0].min()
-names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit"]
+names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit", "fin_beg",
+         "fin_end", "arrived", "part_beg"]
 print(f"M={M} K={K} T={T} event time {s.elapsed_time(e)*1e3:.1f} us, CTAs {used.sum()}")
 for k, nm in enumerate(names):
     col = (t[:, k] - t0) / 1e3
     print(f"{nm:10s} min {col.min():7.2f}  med {sorted(col)[len(col)//2]:7.2f}  max {col.max():7.2f} us")
+order = (t[:, 8] - t0).argsort()[::-1][:6]
+print("slowest CTAs (us):", " ".join(names))
+for c in order:
+    print(c, " ".join(f"{(t[c, k] - t0) / 1e3 if t[c, k] > 0 else -1:6.2f}" for k in range(len(names))))
