@@ -431,8 +431,17 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   const long long units = (long long)p.m_tiles * p.n_tiles * p.k_blocks;
   if (units > (1LL << 30)) return 1;
   p.units = (int)units;
-  // >= 8 k-blocks per CTA: bounds the contributors of a split tile (finisher latency) on small shapes
-  p.grid = (int)std::max<long long>(1, std::min<long long>(units / 8, num_sms));
+  // Work split.  tiles <= #SM: plain split-K with s equal K-ranges per tile (grid = tiles * s, each CTA
+  // inside ONE tile, all contributors of a tile finish together -> a single short fix-up at the end).
+  // tiles > #SM: stream-K over all SMs.  Both keep >= 8 k-blocks per CTA so a split tile has few
+  // contributors.  (The stream-K formula with grid = tiles * s reproduces the split-K ranges.)
+  const long long tiles = (long long)p.m_tiles * p.n_tiles;
+  if (tiles <= num_sms) {
+    long long s = std::max<long long>(1, std::min<long long>(num_sms / tiles, p.k_blocks / 8));
+    p.grid = (int)(tiles * s);
+  } else {
+    p.grid = (int)std::max<long long>(1, std::min<long long>(units / 8, num_sms));
+  }
   p.ids = ids;
   p.tab = tab;
   p.arena = arena;
