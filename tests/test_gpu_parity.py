@@ -379,3 +379,43 @@ def test_error_paths(dev):
     # T = 0 is a no-op
     bd.bdlora_column_forward(pool, X[:0], W, ids[:0], Y[:0], ws)
     pool.close()
+
+
+# ----------------------------------------------------------------------------- launch paths
+
+@pytest.mark.parametrize("pdl", [True, False])
+def test_pdl_on_off_identical(dev, pdl):
+    """Programmatic-dependent-launch chaining changes only scheduling, never values."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.arch_projections("llama-3.1-8b")[2]
+    case = H.make_case(81, proj, "bd", 8, 5, ranks=[16, 32])
+    bd.bdlora_set_pdl(pdl)
+    try:
+        y = run_column(case, 3, dev)
+    finally:
+        bd.bdlora_set_pdl(True)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", 8)
+    _assert_tol(_np(y), ol.column_device_output(ref_full, 8, 3), f"pdl={pdl}")
+
+
+def test_cuda_core_gemv_path_k_not_multiple_of_64(dev):
+    """K % 64 != 0 takes the CUDA-core GEMV kernel (still on the GPU): parity on a ragged K."""
+    proj = synth.Projection("odd", "column", 200, (96, 32))
+    case = H.make_case(82, proj, "bd", 2, 7, ranks=[8, 16])
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", 2)
+    for i in range(2):
+        _assert_tol(_np(run_column(case, i, dev)), ol.column_device_output(ref_full, 2, i), f"rank {i}")
+
+
+@pytest.mark.parametrize("T", [129, 300])
+def test_prefill_token_tiles(dev, T):
+    """More tokens than one 256-wide token tile (n_tiles > 1) and a ragged token tail, segments of
+    requests (SGMV-shaped ids), TP=8 rank 3 of 8B gate_up-like shapes (narrowed)."""
+    proj = synth.Projection("gate_up", "column", 1024, (2048, 2048))
+    ids = synth.ids_segments(T, 3)
+    case = H.make_case(83 + T, proj, "bd", 8, T, ranks=[64, 32, 64], ids=ids)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", 8)
+    _assert_tol(_np(run_column(case, 3, dev)), ol.column_device_output(ref_full, 8, 3), f"T={T}")
