@@ -419,3 +419,100 @@ def test_prefill_token_tiles(dev, T):
     case = H.make_case(83 + T, proj, "bd", 8, T, ranks=[64, 32, 64], ids=ids)
     ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", 8)
     _assert_tol(_np(run_column(case, 3, dev)), ol.column_device_output(ref_full, 8, 3), f"T={T}")
+
+
+# ----------------------------------------------------------------------------- full-size, sampled
+
+def _sampled_check(y_dev, X, W_cols, col_index, ads_dense, ids, rng, n_samples=96, what=""):
+    """Compare n_samples random outputs of a full-size device output against the oracle computed one by
+    one (oracle.lora_layer_sampled): W_cols[:, q] is the base weight column of local output column
+    col_index[q] (paper orientation)."""
+    T, M = y_dev.shape
+    ts = rng.integers(0, T, size=n_samples)
+    cs = rng.integers(0, M, size=n_samples)
+    got = y_dev[ts, cs].astype(np.float64)
+    # oracle.lora_layer_sampled, one output at a time (dW column = A B[:, c] materialised)
+    out = np.empty(n_samples)
+    for k, (t, c) in enumerate(zip(ts, cs)):
+        out[k] = ol.lora_layer_sampled(X, W_cols, ads_dense, ids, [(int(t), int(col_index[c]))])[0]
+    _assert_tol(got, out, what)
+
+
+def test_full_size_bench_config_8b_decode(dev):
+    """The bench's own workload at full size and in its launch configuration: Llama-3.1-8B layer,
+    decode T=1, rank 16, TP=1 -- every projection, sampled outputs vs the oracle one by one."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    rng_s = np.random.default_rng(5)
+    for k, proj in enumerate(synth.arch_projections("llama-3.1-8b")):
+        case = H.make_case(900 + k, proj, "bd", 1, 1, ranks=[16], ids=np.zeros(1, np.int32))
+        pool = H.make_pool(case, 0)
+        X, W, ids = H.device_inputs(case, 0, dev)
+        Y = torch.empty(1, pool.m_loc, dtype=torch.bfloat16, device=dev)
+        ws = bd.make_workspace(pool, 1)
+        if proj.parallel == "column":
+            bd.bdlora_column_forward(pool, X, W, ids, Y, ws)
+        else:
+            bd.bdlora_row_forward(pool, None, X, W, ids, Y, ws)
+        torch.cuda.synchronize()
+        ads = case.oracle_adapters()
+        Wf = case.W.f64
+        if proj.parallel == "column":
+            # local columns are [q|k|v] or [gate|up] = full columns at N=1; per slice factors
+            y = _np(Y)
+            col0 = 0
+            for j, dj in enumerate(proj.d_out):
+                dense = {a: (d["scale"],) + ol.dense_factors("column", "bd", d["A"], d["B"], 1)[j] for a, d in ads.items()}
+                _sampled_check(y[:, col0:col0 + dj], case.X.f64, Wf[:, col0:col0 + dj], np.arange(dj), dense,
+                               case.ids, rng_s, 48, f"{proj.name} slice {j}")
+                col0 += dj
+        else:
+            dense = {a: (d["scale"],) + ol.dense_factors("row", "bd", d["A"], d["B"], 1)[0] for a, d in ads.items()}
+            _sampled_check(_np(Y), case.X.f64, Wf, np.arange(proj.d_out[0]), dense, case.ids, rng_s, 96, proj.name)
+        pool.close()
+
+
+def test_full_size_multitenant_70b_gate_up_tp8(dev):
+    """configs[4] at full size on one emulated rank: Llama-3.1-70B gate_up (8192 -> 2 x 28672) at TP=8,
+    64 decode tokens over 128 resident adapters of mixed rank {8..128}, uniform ids; sampled outputs."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.arch_projections("llama-3.1-70b")[2]
+    n, i, T = 8, 5, 64
+    ranks = [[8, 16, 32, 64, 128][k % 5] for k in range(128)]
+    rng = synth.rng_for(910, 1)
+    ids = synth.ids_uniform(rng, T, 128)
+    ads = {a: synth.make_adapter(rng, proj, "bd", r, n, synth.rs_scale(16.0, r, n, "bd")) for a, r in enumerate(ranks)}
+    X = synth.make_x(rng, T, proj.d_in)
+    # only device i's base columns are generated (column-parallel: W_i = column block i of each slice)
+    w_loc = [synth.bf16_normal(rng, (proj.d_in, dj // n), 1 / np.sqrt(proj.d_in)) for dj in proj.d_out]
+    pool = bd.bdlora_create_pool(bd.COLUMN, bd.SHARD_BD, n, i, proj.d_in, proj.d_out, 128, 128, device=0)
+    for a, ad in ads.items():
+        bd.bdlora_load_adapter(pool, a, ad.rank, ad.scale, [H.torch_bf16(x.bits) for x in ad.A],
+                               [H.torch_bf16(x.bits) for x in ad.B])
+    Wt = H.torch_bf16(np.ascontiguousarray(np.concatenate([w.bits for w in w_loc], axis=1).T), dev)
+    Xd = H.torch_bf16(X.bits, dev)
+    Y = torch.empty(T, pool.m_loc, dtype=torch.bfloat16, device=dev)
+    bd.bdlora_column_forward(pool, Xd, Wt, torch.from_numpy(ids).to(dev), Y, bd.make_workspace(pool, T))
+    torch.cuda.synchronize()
+    y = _np(Y)
+    used = sorted(set(ids.tolist()))
+    rng_s = np.random.default_rng(6)
+    col0 = 0
+    for j, dj in enumerate(proj.d_out):
+        w = dj // n
+        dense = {}
+        for a in used:
+            A, B = ol.dense_factors("column", "bd", [x.f64 for x in ads[a].A], [x.f64 for x in ads[a].B], n)[j]
+            dense[a] = (ads[a].scale, A, B)
+        # local column c of slice j is full column i*w + c; W_cols holds only the local block
+        Wfull_cols = np.zeros((proj.d_in, dj))
+        Wfull_cols[:, i * w:(i + 1) * w] = w_loc[j].f64
+        _sampled_check(y[:, col0:col0 + w], X.f64, Wfull_cols, i * w + np.arange(w), dense, ids, rng_s, 64,
+                       f"70B gate_up slice {j}")
+        col0 += w
+    pool.close()
