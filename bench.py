@@ -124,6 +124,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def reduce_max(x: float, device=None) -> float:
+    """Max over ranks of a host float (timings are reported as the max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -302,48 +314,43 @@ def time_layer(bd, torch, layer, comm, ids, steps, warmup, use_graph, barrier):
         per.append(ms / steps * 1e3)
     return total, per, launches
 def time_e2e(bd, torch, layer, comm, ids_np, steps, warmup, barrier):
-    """Same step through the public API with HOST buffers: pinned H2D of every projection's input and
-    the ids, the four forwards, D2H of every output -- all inside the timed region (graph-captured)."""
+    """Same step through the public API with HOST buffers: one pinned H2D copy of the step's inputs
+    (every projection's activations + the ids, packed), the four forwards, one D2H copy of the four
+    outputs -- all inside the timed region (graph-captured).  Returns (ms, h2d bytes, d2h bytes)."""
     dev = layer[0].X.device
     T = layer[0].X.shape[0]
-    hx = [torch.empty_like(p.X, device="cpu").pin_memory() for p in layer]
-    for h, p in zip(hx, layer):
-        h.copy_(p.X.cpu())
-    hid = torch.from_numpy(ids_np.copy()).pin_memory()
-    hy = [torch.empty_like(p.Y, device="cpu").pin_memory() for p in layer]
-    dx = [torch.empty_like(p.X) for p in layer]
-    did = torch.empty(T, dtype=torch.int32, device=dev)
-    h2d = sum(h.numel() * h.element_size() for h in hx) + hid.numel() * 4
-    d2h = sum(h.numel() * h.element_size() for h in hy)
+    xs = [p.X.numel() for p in layer]
+    ys = [p.Y.numel() for p in layer]
+    nin = sum(xs) + 2 * T  # bf16 elements; ids (int32) packed as 2 bf16 slots each
+    h_in = torch.empty(nin, dtype=torch.bfloat16).pin_memory()
+    d_in = torch.empty(nin, dtype=torch.bfloat16, device=dev)
+    off = 0
+    dx = []
+    for p, n in zip(layer, xs):
+        h_in[off:off + n].copy_(p.X.reshape(-1).cpu())
+        dx.append(d_in[off:off + n].view(p.X.shape))
+        off += n
+    h_in[off:off + 2 * T].view(torch.int32).copy_(torch.from_numpy(ids_np.copy()))
+    did = d_in[off:off + 2 * T].view(torch.int32)
+    d_out = torch.empty(sum(ys), dtype=torch.bfloat16, device=dev)
+    h_out = torch.empty(sum(ys), dtype=torch.bfloat16).pin_memory()
+    dy = []
+    off = 0
+    for p, n in zip(layer, ys):
+        dy.append(d_out[off:off + n].view(p.Y.shape))
+        off += n
 
     def step(k):
-        did.copy_(hid, non_blocking=True)
-        for h, d in zip(hx, dx):
-            d.copy_(h, non_blocking=True)
-        for p, d in zip(layer, dx):
-            p.run(bd, comm, did, k, X=d)
-        for h, p in zip(hy, layer):
-            h.copy_(p.Y, non_blocking=True)
+        d_in.copy_(h_in, non_blocking=True)
+        for p, x, y in zip(layer, dx, dy):
+            p.run(bd, comm, did, k, X=x, Y=y)
+        h_out.copy_(d_out, non_blocking=True)
 
     for w in range(warmup):
         step(w)
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        for k in range(steps):
-            step(k)
-    g.replay()
-    torch.cuda.synchronize()
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
-    start.record()
-    g.replay()
-    end.record()
-    torch.cuda.synchronize()
-    barrier()
-    return start.elapsed_time(end), h2d, d2h
+    ms = graph_time(torch, step, steps, barrier)
+    return ms, nin * 2, sum(ys) * 2
 
 
 # ============================================================================ oracle legs
@@ -456,12 +463,7 @@ def run_ours(args, wl):
     clocks.start()
     total_ms, per, launches = time_layer(bd, torch, layer, comm, ids, args.steps, args.warmup, not args.no_graph, barrier)
     clk = clocks.stop()
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = reduce_max(total_ms, dev)
     ms_step = total_ms / args.steps
     value = T / (ms_step * 1e-3)
     names = [p.proj.name for p in layer]
@@ -502,12 +504,7 @@ def run_ours(args, wl):
     if not args.skip_slora:
         sl_layer, _ = build_layer(bd, torch, wl, "slora", n, rank, dev, share_w=layer)
         s_total, s_per, _ = time_layer(bd, torch, sl_layer, comm, ids, args.steps, args.warmup, not args.no_graph, barrier)
-        if world > 1:
-            import torch.distributed as dist
-
-            t = torch.tensor([s_total], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            s_total = float(t.item())
+        s_total = reduce_max(s_total, dev)
         slora = {"ms_per_step": s_total / args.steps, "tokens_per_s": T / (s_total / args.steps * 1e-3),
                  "proj_us": dict(zip(names, s_per)),
                  "bd_speedup": (s_total / total_ms)}
@@ -519,12 +516,7 @@ def run_ours(args, wl):
 
     # ---------------- e2e through the public API with host buffers ----------------
     e2e_ms, h2d, d2h = time_e2e(bd, torch, layer, comm, ids_np, args.steps, args.warmup, barrier)
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = reduce_max(e2e_ms, dev)
     e2e = {"value": T / (e2e_ms / args.steps * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps}
     collectives = bd.bdlora_comm_stats(comm) if comm is not None else None

@@ -140,21 +140,30 @@ def bdlora_comm_init(uid: bytes, nranks: int, rank: int, device: int) -> Comm:
     return Comm(h.value, nranks, rank, device)
 
 
-def comm_from_process_group(device: int, group=None) -> Optional[Comm]:
-    """NCCL bootstrap over torch.distributed: rank 0 draws the unique id, broadcast, init (SURVEY §8(e))."""
+def broadcast_unique_id(group=None, device=None) -> bytes:
+    """Rank 0 of the process group draws an NCCL unique id (bdlora_comm_unique_id) and broadcasts
+    the 128 bytes over torch.distributed (any backend: gloo on CPU, nccl on `device`)."""
     torch = _torch()
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    if world == 1:
-        return None
     uid = bdlora_comm_unique_id() if rank == 0 else bytes(128)
     t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).clone()
     if dist.get_backend(group) == "nccl":
         t = t.to(torch.device("cuda", device))
     dist.broadcast(t, src=0, group=group)
-    return bdlora_comm_init(bytes(t.cpu().numpy().tobytes()), world, rank, device)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def comm_from_process_group(device: int, group=None) -> Optional[Comm]:
+    """NCCL bootstrap over torch.distributed: rank 0 draws the unique id, broadcast, init (SURVEY §8(e))."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    if world == 1:
+        return None
+    uid = broadcast_unique_id(group, device)
+    return bdlora_comm_init(uid, world, dist.get_rank(group), device)
 
 
 def bdlora_comm_destroy(comm: Comm) -> None:
