@@ -29,6 +29,8 @@ constexpr int kUmmaThreads = 192;
 
 struct UmmaParams {
   int M, K, T;
+  int rs_max;  // fused shrink: rank rows per slot capacity
+  const __nv_bfloat16* X;
   int m_tiles, n_tiles, k_blocks;
   int units, grid;
   const int* ids;
@@ -40,6 +42,9 @@ struct UmmaParams {
   float* part;    // [grid][2][128][BN] fp32 split-tile partials (slot 0: a CTA's first segment, 1: last)
   int* tile_cnt;  // [m_tiles * n_tiles], zero between launches
   int pdl;
+  int fuse;          // 1: the epilogue warps also compute v (fused shrink); 0: v comes from a prior kernel
+  float* v_out;      // fused mode: v [T][J][Rc] written here (== v)
+  int* sync;         // fused mode: [0] unit claim counter, [1] units done, [2] CTAs exited (zero between launches)
   long long* trace;  // optional per-CTA timestamps (ns, %globaltimer) for profiling; nullptr = off
 };
 
@@ -67,7 +72,7 @@ struct UmmaSmem {
   static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kBytes = kBarOff + 256 + 2048 + 1024;  // + barriers/flags, ids/leaders, alignment slack
+  static constexpr int kBytes = kBarOff + 256 + 4096 + 128 + 1024;  // + barriers/flags, ids/leaders/shrink, slack
 };
 
 template <int BN>
@@ -87,6 +92,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_last = (int*)(tmem_holder + 1);
   int* s_ids = (int*)(smem + S::kBarOff + 256);  // [BN] adapter ids of the current token tile
   int* s_lead = s_ids + 256;                     // [BN] group leader of each token in its 16-chunk
+  int* s_fids = s_lead + 256;                    // [T <= 256] all ids (fused shrink)
+  int* s_mem = s_fids + 256;                     // [T] members of the current adapter group
+  float* s_red = (float*)(s_mem + 256);          // [4][4] cross-warp partial dots
+  int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -197,8 +206,84 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..127
-    if (p.pdl) ptx::pdl_wait();         // the preceding kernel (shrink: v) is complete and visible;
-                                        // also orders our Y writes after every earlier reader
+    if (p.pdl) ptx::pdl_wait();         // the preceding kernel is complete and visible (X, ids, and v
+                                        // when it was a shrink); also orders our Y writes after it
+    if (p.fuse) {
+      // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
+      // Units (leader token t, slice j, rank row k) are CLAIMED dynamically (atomic counter) by the
+      // epilogue warps of whichever CTAs are resident, while the producer/MMA warps stream W; a unit is
+      // computed once per DISTINCT adapter (leader = first token with that id) for all its tokens.
+      for (int t = etid; t < p.T; t += 128) s_fids[t] = __ldg(p.ids + t);
+      ptx::named_bar_sync(1, 128);
+      const int Js = p.g.J, rsm = p.rs_max;
+      const int U_s = p.T * Js * rsm;
+      const int warp_e = etid >> 5;
+      for (;;) {
+        if (etid == 0) s_misc[0] = atomicAdd(p.sync + 0, 1);
+        ptx::named_bar_sync(1, 128);
+        const int us = s_misc[0];
+        if (us >= U_s) break;
+        const int t_lead = us / (Js * rsm), j = (us / rsm) % Js, k = us % rsm;
+        const int a = s_fids[t_lead];
+        bool leader = a >= 0;
+        for (int t2 = 0; t2 < t_lead && leader; ++t2) leader = (s_fids[t2] != a);
+        const SlotEntry* e = leader ? p.tab + a : nullptr;
+        if (leader && k < e->rs) {
+          if (warp_e == 0) {  // members of this adapter group, token order
+            int cnt = 0;
+            for (int base = t_lead; base < p.T; base += 32) {
+              const int t2 = base + lane;
+              const unsigned m = __ballot_sync(0xffffffffu, t2 < p.T && s_fids[t2] == a);
+              if (t2 < p.T && s_fids[t2] == a) s_mem[cnt + __popc(m & ((1u << lane) - 1u))] = t2;
+              cnt += __popc(m);
+            }
+            if (lane == 0) s_misc[1] = cnt;
+          }
+          ptx::named_bar_sync(1, 128);
+          const int cnt = s_misc[1];
+          const __nv_bfloat16* Ar = p.arena + e->offA[j] + (size_t)k * p.K;
+          for (int m0 = 0; m0 < cnt; m0 += 4) {
+            float acc4[4] = {0.f, 0.f, 0.f, 0.f};
+            int tok[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) tok[m] = (m0 + m < cnt) ? s_mem[m0 + m] : -1;
+#pragma unroll 4
+            for (int d = etid * 8; d < p.K; d += 128 * 8) {
+              float af[8];
+              bf16x8_to_f32(ld_cached_u4(Ar + d), af);
+#pragma unroll
+              for (int m = 0; m < 4; ++m) {
+                if (tok[m] >= 0) {
+                  float xf[8];
+                  bf16x8_to_f32(ld_cached_u4(p.X + (size_t)tok[m] * p.K + d), xf);
+#pragma unroll
+                  for (int q2 = 0; q2 < 8; ++q2) acc4[m] = fmaf(af[q2], xf[q2], acc4[m]);
+                }
+              }
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const float sm = warp_sum(acc4[m]);
+              if (lane == 0) s_red[warp_e * 4 + m] = sm;
+            }
+            ptx::named_bar_sync(1, 128);
+            if (etid < 4 && tok[etid & 3] >= 0) {
+              const int m = etid;
+              const float sm = (s_red[m] + s_red[4 + m]) + (s_red[8 + m] + s_red[12 + m]);
+              p.v_out[((size_t)s_mem[m0 + m] * Js + j) * p.g.Rc + k] = e->scale * sm;
+            }
+            ptx::named_bar_sync(1, 128);
+          }
+        }
+        if (etid == 0) ptx::atom_add_acq_rel_gpu(p.sync + 1, 1);  // publishes this unit's v (release)
+        ptx::named_bar_sync(1, 128);
+      }
+      // every unit of the launch published before any expand reads v
+      if (etid == 0) {
+        while (ptx::ld_acquire_gpu(p.sync + 1) < U_s) __nanosleep(64);
+      }
+      ptx::named_bar_sync(1, 128);
+    }
     int acc = 0;
     uint32_t acc_phase = 0;
     int cur_nt = -1;
@@ -336,7 +421,14 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if (threadIdx.x == 0) UMMA_TRACE(8);
+  if (threadIdx.x == 0) {
+    UMMA_TRACE(8);
+    if (p.fuse && atomicAdd(p.sync + 2, 1) == (int)gridDim.x - 1) {  // last CTA out re-arms the counters
+      p.sync[0] = 0;
+      p.sync[1] = 0;
+      p.sync[2] = 0;
+    }
+  }
   if (warp == 1) ptx::tmem_dealloc<S::kTmemCols>(tmem_base);
 }
 
@@ -347,13 +439,16 @@ inline long long* g_umma_trace = nullptr;  // profiling hook (bdlora_debug_trace
 
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
 
+constexpr int kFuseMaxT = 256;  // fused shrink handles decode-sized batches (ids staged in smem)
+
+// Workspace: [sync: 3 ints, 256 B][tile counters][split-tile partials]
 inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
   const int BN = umma_bn_for(T);
   const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM;
   const int n_tiles = (T + BN - 1) / BN;
   size_t part = (size_t)num_sms * 2 * BN * kUmmaBM * sizeof(float);
   size_t cnt = (size_t)m_tiles * n_tiles * sizeof(int);
-  return ((cnt + 255) / 256) * 256 + part;
+  return 256 + ((cnt + 255) / 256) * 256 + part;
 }
 
 inline bool umma_eligible(const Geom& g, int T) { return T >= 1 && g.K % kUmmaBK == 0 && g.K >= kUmmaBK; }
@@ -418,8 +513,9 @@ inline int umma_launch_bn(const UmmaParams& p0, const __nv_bfloat16* X, const __
 // Returns 0 on launch, non-zero if the shape is not handled here.
 inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_bfloat16* W, const int* ids,
                        const SlotEntry* tab, const __nv_bfloat16* arena, const float* v, __nv_bfloat16* Y, void* ws,
-                       int num_sms, cudaStream_t st, int pdl = 0) {
+                       int num_sms, cudaStream_t st, int pdl = 0, float* v_fused = nullptr, int rs_max = 0) {
   if (!umma_eligible(g, T)) return 1;
+  if (v_fused && T > kFuseMaxT) return 1;
   const int BN = umma_bn_for(T);
   UmmaParams p;
   p.M = g.M;
@@ -449,8 +545,14 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.v = v;
   p.Y = Y;
   const size_t cnt_bytes = (((size_t)p.m_tiles * p.n_tiles * sizeof(int)) + 255) / 256 * 256;
-  p.tile_cnt = (int*)ws;
-  p.part = (float*)((char*)ws + cnt_bytes);
+  p.sync = (int*)ws;
+  p.tile_cnt = (int*)((char*)ws + 256);
+  p.part = (float*)((char*)ws + 256 + cnt_bytes);
+  p.X = X;
+  p.fuse = v_fused ? 1 : 0;
+  p.v_out = v_fused;
+  p.rs_max = rs_max;
+  if (v_fused) p.v = v_fused;
   p.pdl = pdl;
   p.trace = g_umma_trace;
   switch (BN) {

@@ -737,6 +737,18 @@ int bdlora_base_expand(bdlora_pool* p, const void* X, int64_t T, const void* W, 
 static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y, void* ws,
                     cudaStream_t st) {
   float* v = ws_v(p, ws, T);
+  if (bdl::umma_eligible(p->g, (int)T) && T <= bdl::kFuseMaxT) {
+    // decode: ONE kernel -- the shrink runs in the GEMM's epilogue warps while the weights stream
+    const WsLayout L = ws_layout(p, T);
+    int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, (int)T, (const __nv_bfloat16*)W, ids, p->d_tab,
+                              (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
+                              p->num_sms, st, g_pdl, v, p->rs_max);
+    if (rc == 0) {
+      count_launch();
+      CU_TRY(cudaGetLastError());
+      return BDLORA_OK;
+    }
+  }
   ST_TRY(launch_shrink(p, X, (int)T, ids, v, st));
   // programmatic dependent launch: the GEMM streams W while the shrink runs; only its epilogue waits
   return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st);
