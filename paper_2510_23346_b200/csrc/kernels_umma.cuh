@@ -208,13 +208,45 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     const int etid = threadIdx.x - 64;  // 0..127
     if (p.pdl) ptx::pdl_wait();         // the preceding kernel is complete and visible (X, ids, and v
                                         // when it was a shrink); also orders our Y writes after it
+    if (p.T <= kFuseMaxT) {
+      // ---- L2 prefetch of the LoRA data this launch gathers (tiny, latency-critical): issued now, at the
+      // start of the weight stream, so the shrink's A rows and the expand's B rows hit L2 later ----------
+      for (int t = etid; t < p.T; t += 128) s_fids[t] = __ldg(p.ids + t);
+      ptx::named_bar_sync(1, 128);
+      const int mt_a = (u_lo / p.k_blocks) % p.m_tiles;
+      const int mt_b = ((u_hi - 1) / p.k_blocks) % p.m_tiles;
+      for (int t = 0; t < p.T; ++t) {  // uniform loop over distinct adapters (leaders)
+        const int a = s_fids[t];
+        if (a < 0) continue;
+        bool leader = true;
+        for (int t2 = 0; t2 < t && leader; ++t2) leader = (s_fids[t2] != a);
+        if (!leader) continue;
+        const SlotEntry* e = p.tab + a;
+        for (int mt = mt_a; mt <= mt_b; ++mt) {  // B rows of my output columns
+          const int n0 = mt * kUmmaBM;
+          for (int jj = 0; jj < p.g.J; ++jj) {
+            const int lo = max(n0, p.g.e_lo[jj]), hi = min(n0 + kUmmaBM, p.g.e_hi[jj]);
+            if (lo >= hi) continue;
+            const int ldb = p.g.e_hi[jj] - p.g.e_lo[jj];
+            for (int k = etid; k < e->re; k += 128)
+              ptx::prefetch_l2_bulk(p.arena + e->offB[jj] + (size_t)k * ldb + (lo - p.g.e_lo[jj]), (hi - lo) * 2);
+          }
+        }
+        if (p.fuse) {  // A rows of the shrink units statically associated with this CTA
+          for (int jj = 0; jj < p.g.J; ++jj)
+            for (int k = 0; k < e->rs; ++k) {
+              const int us = (t * p.g.J + jj) * p.rs_max + k;
+              if (us % (int)gridDim.x == cta && (k & 127) == etid)
+                ptx::prefetch_l2_bulk(p.arena + e->offA[jj] + (size_t)k * p.K, p.K * 2);
+            }
+        }
+      }
+    }
     if (p.fuse) {
       // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
       // Units (leader token t, slice j, rank row k) are CLAIMED dynamically (atomic counter) by the
       // epilogue warps of whichever CTAs are resident, while the producer/MMA warps stream W; a unit is
       // computed once per DISTINCT adapter (leader = first token with that id) for all its tokens.
-      for (int t = etid; t < p.T; t += 128) s_fids[t] = __ldg(p.ids + t);
-      ptx::named_bar_sync(1, 128);
       const int Js = p.g.J, rsm = p.rs_max;
       const int U_s = p.T * Js * rsm;
       const int warp_e = etid >> 5;
@@ -280,7 +312,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       }
       // every unit of the launch published before any expand reads v
       if (etid == 0) {
+        UMMA_TRACE(13);
         while (ptx::ld_acquire_gpu(p.sync + 1) < U_s) __nanosleep(64);
+        UMMA_TRACE(14);
       }
       ptx::named_bar_sync(1, 128);
     }

@@ -143,6 +143,14 @@ __device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
   return old;
 }
 
+// Bulk L2 prefetch (no smem destination): pulls a small gather target into L2 ahead of use so the
+// dependent loads that follow hit L2 instead of queueing behind the weight stream in HBM.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  uintptr_t a = (uintptr_t)p & ~(uintptr_t)15;
+  uint32_t n = (uint32_t)(((uintptr_t)p + bytes - a + 15) & ~(uintptr_t)15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -28,10 +28,14 @@ tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
 for i in range(6):
     bd.bdlora_base_expand(pool, X, Ws[i % nrep], ids, v, Y, ws)
 torch.cuda.synchronize()
+fused = len(sys.argv) > 4 and sys.argv[4] == "fused"
 bd.bdlora_debug_trace(tr)
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
-bd.bdlora_base_expand(pool, X, Ws[0], ids, v, Y, ws)
+if fused:
+    bd.bdlora_column_forward(pool, X, Ws[0], ids, Y, ws)
+else:
+    bd.bdlora_base_expand(pool, X, Ws[0], ids, v, Y, ws)
 e.record()
 torch.cuda.synchronize()
 bd.bdlora_debug_trace(None)
@@ -40,7 +44,7 @@ used = t[:, 0] > 0
 t = t[used]
 t0 = t[:, 0].min()
 names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit", "fin_beg",
-         "fin_end", "arrived", "part_beg"]
+         "fin_end", "arrived", "part_beg", "shr_done", "v_ready"]
 print(f"M={M} K={K} T={T} event time {s.elapsed_time(e)*1e3:.1f} us, CTAs {used.sum()}")
 for k, nm in enumerate(names):
     col = (t[:, k] - t0) / 1e3
