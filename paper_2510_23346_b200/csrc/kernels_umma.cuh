@@ -26,6 +26,7 @@ namespace bdl {
 constexpr int kUmmaBM = 128;
 constexpr int kUmmaBK = 64;
 constexpr int kUmmaThreads = 192;
+constexpr int kFuseMaxT = 256;  // fused shrink / LoRA prefetch handle decode-sized batches (ids staged in smem)
 
 struct UmmaParams {
   int M, K, T;
@@ -472,8 +473,6 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
 inline long long* g_umma_trace = nullptr;  // profiling hook (bdlora_debug_trace)
 
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
-
-constexpr int kFuseMaxT = 256;  // fused shrink handles decode-sized batches (ids staged in smem)
 
 // Workspace: [sync: 3 ints, 256 B][tile counters][split-tile partials]
 inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
