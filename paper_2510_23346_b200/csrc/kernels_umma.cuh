@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     const int etid = threadIdx.x - 64;  // 0..127
     if (p.pdl) ptx::pdl_wait();         // the preceding kernel is complete and visible (X, ids, and v
                                         // when it was a shrink); also orders our Y writes after it
+    if (p.fuse && etid == 0) s_misc[0] = atomicAdd(p.sync + 0, 1);  // fused-shrink arrival ticket (below)
     if (p.T <= kFuseMaxT) {
       // ---- L2 prefetch of the LoRA data this launch gathers (tiny, latency-critical): issued now, at the
       // start of the weight stream, so the shrink's A rows and the expand's B rows hit L2 later ----------
@@ -233,29 +234,23 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               ptx::prefetch_l2_bulk(p.arena + e->offB[jj] + (size_t)k * ldb + (lo - p.g.e_lo[jj]), (hi - lo) * 2);
           }
         }
-        if (p.fuse) {  // A rows of the shrink units statically associated with this CTA
-          for (int jj = 0; jj < p.g.J; ++jj)
-            for (int k = 0; k < e->rs; ++k) {
-              const int us = (t * p.g.J + jj) * p.rs_max + k;
-              if (us % (int)gridDim.x == cta && (k & 127) == etid)
-                ptx::prefetch_l2_bulk(p.arena + e->offA[jj] + (size_t)k * p.K, p.K * 2);
-            }
-        }
       }
     }
     if (p.fuse) {
       // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
-      // Units (leader token t, slice j, rank row k) are CLAIMED dynamically (atomic counter) by the
-      // epilogue warps of whichever CTAs are resident, while the producer/MMA warps stream W; a unit is
-      // computed once per DISTINCT adapter (leader = first token with that id) for all its tokens.
+      // Units (leader token t, slice j, rank row k) are computed by the epilogue warps while the
+      // producer/MMA warps stream W; a unit is computed once per DISTINCT adapter (leader = first token
+      // with that id) for all its tokens.
       const int Js = p.g.J, rsm = p.rs_max;
       const int U_s = p.T * Js * rsm;
       const int warp_e = etid >> 5;
-      for (;;) {
-        if (etid == 0) s_misc[0] = atomicAdd(p.sync + 0, 1);
-        ptx::named_bar_sync(1, 128);
-        const int us = s_misc[0];
-        if (us >= U_s) break;
+      // units are owned by ARRIVAL TICKET: a CTA draws its ticket once it runs, so every unit belongs to a
+      // resident CTA (no deadlock whatever the residency) and costs one atomic per CTA, not per unit
+      ptx::named_bar_sync(1, 128);
+      const int ticket = s_misc[0];
+      int mine = 0;
+      for (int us = ticket; us < U_s; us += (int)gridDim.x) {
+        ++mine;
         const int t_lead = us / (Js * rsm), j = (us / rsm) % Js, k = us % rsm;
         const int a = s_fids[t_lead];
         bool leader = a >= 0;
@@ -308,9 +303,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             ptx::named_bar_sync(1, 128);
           }
         }
-        if (etid == 0) ptx::atom_add_acq_rel_gpu(p.sync + 1, 1);  // publishes this unit's v (release)
-        ptx::named_bar_sync(1, 128);
       }
+      ptx::named_bar_sync(1, 128);
+      if (etid == 0 && mine) ptx::atom_add_acq_rel_gpu(p.sync + 1, mine);  // publishes my v (release)
       // every unit of the launch published before any expand reads v
       if (etid == 0) {
         UMMA_TRACE(13);
