@@ -21,6 +21,9 @@
 #include "common.cuh"
 #include "ptx.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace bdl {
 
 constexpr int kUmmaBM = 128;
@@ -43,6 +46,7 @@ struct UmmaParams {
   float* part;    // [grid][2][128][BN] fp32 split-tile partials (slot 0: a CTA's first segment, 1: last)
   int* tile_cnt;  // [m_tiles * n_tiles], zero between launches
   int pdl;
+  int nstages;       // ring stages actually used (<= kStages): bounds the bytes in flight per SM
   int fuse;          // 1: the epilogue warps also compute v (fused shrink); 0: v comes from a prior kernel
   float* v_out;      // fused mode: v [T][J][Rc] written here (== v)
   int* sync;         // fused mode: [0] unit claim counter, [1] units done, [2] CTAs exited (zero between launches)
@@ -138,7 +142,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const uint64_t pol_w = ptx::policy_evict_first();
       const uint64_t pol_x = ptx::policy_evict_last();
       const int nu = u_hi - u_lo;
-      const int P = min(nu, S::kStages);
+      const int NS = p.nstages;
+      const int P = min(nu, NS);
       for (int idx = 0; idx < P; ++idx) {
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, mt = tile % p.m_tiles;
         ptx::mbar_arrive_expect_tx(&full[idx], S::kStageBytes);
@@ -150,8 +155,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, nt = tile / p.m_tiles;
         ptx::tma_load_2d(sX + idx * S::kXBytes, &tmX, &full[idx], kb * kUmmaBK, nt * BN, pol_x);
       }
-      int stage = (P == S::kStages) ? 0 : P;
-      uint32_t phase = (P == S::kStages) ? 1u : 0u;
+      int stage = (P == NS) ? 0 : P;
+      uint32_t phase = (P == NS) ? 1u : 0u;
       for (int idx = P; idx < nu; ++idx) {
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks;
         const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
         ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
         ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
-        if (++stage == S::kStages) {
+        if (++stage == p.nstages) {
           stage = 0;
           phase ^= 1;
         }
@@ -190,7 +195,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           for (int k = 0; k < kUmmaBK / 16; ++k)  // UMMA_K = 16 bf16 = 32 B -> +2 in the >>4 address field
             ptx::mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           ptx::mma_commit(&empty[stage]);
-          if (++stage == S::kStages) {
+          if (++stage == p.nstages) {
             stage = 0;
             phase ^= 1;
           }
@@ -511,9 +516,24 @@ inline bool encode_kmajor(CUtensorMap* m, const void* base, int K, int rows, int
   return r == CUDA_SUCCESS;
 }
 
+// Ring depth.  Decode is an HBM stream: ~1 us of DRAM latency x 44 GB/s per SM needs ~3-4 stages of 18 KB;
+// deeper rings only queue more bytes in HBM, which inflates the latency of every dependent LoRA load
+// (Little's law) without adding bandwidth.  Override with BDLORA_STAGES for tuning.
+inline int umma_stage_cap(int T) {
+  static int env = -1;
+  if (env < 0) {
+    const char* s = getenv("BDLORA_STAGES");
+    env = s ? std::max(1, atoi(s)) : 0;
+  }
+  if (env > 0) return env;
+  return T <= 64 ? 4 : 64;
+}
+
 template <int BN>
 inline int umma_launch_bn(const UmmaParams& p0, const __nv_bfloat16* X, const __nv_bfloat16* W, cudaStream_t st) {
   using S = UmmaSmem<BN>;
+  UmmaParams p1 = p0;
+  p1.nstages = std::min(S::kStages, umma_stage_cap(p0.T));
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) !=
@@ -534,7 +554,7 @@ inline int umma_launch_bn(const UmmaParams& p0, const __nv_bfloat16* X, const __
   attr[0].val.programmaticStreamSerializationAllowed = p0.pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN>, tmW, tmX, p0) != cudaSuccess) return 4;
+  if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN>, tmW, tmX, p1) != cudaSuccess) return 4;
   return 0;
 }
 
@@ -583,6 +603,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   if (v_fused) p.v = v_fused;
   p.pdl = pdl;
   p.trace = g_umma_trace;
+  p.nstages = 0;  // set per BN below
   switch (BN) {
     case 16: return umma_launch_bn<16>(p, X, W, st);
     case 32: return umma_launch_bn<32>(p, X, W, st);
