@@ -115,10 +115,44 @@ __device__ __forceinline__ float lora_expand_term(int t, int n, int a, const Slo
 // DISTINCT adapter, 16 independent loads in flight; consecutive threads hold consecutive output
 // columns, so every B row segment is read coalesced.  v values are loaded before use and reduced in
 // 4 independent chains (no load->FMA latency chain).
+// B rows of ONE adapter gathered ahead of time (decode fast path: the first 16-token chunk holds a single
+// adapter group, C == 1, re <= 16) so only the v load remains once v is ready.
+struct LoraPre {
+  int a;  // adapter id, -1 = none
+  float b[16];
+};
+
+__device__ __forceinline__ void lora_pre16(LoraPre& pre, int n, int cnt, const int* s_ids, const int* s_lead,
+                                           const SlotEntry* __restrict__ tab,
+                                           const __nv_bfloat16* __restrict__ arena, const Geom& g) {
+  pre.a = -1;
+  if (n >= g.M || g.C != 1) return;
+  int lead = -1;
+  for (int i = 0; i < cnt; ++i) {
+    if (s_lead[i] < 0) continue;
+    if (lead < 0) lead = s_lead[i];
+    if (s_lead[i] != lead) return;  // more than one group: generic path
+  }
+  if (lead < 0) return;
+  const int a = s_ids[lead];
+  int j = 0;
+#pragma unroll
+  for (int q = 1; q < kMaxSlices; ++q)
+    if (q < g.J && n >= g.col0[q]) j = q;
+  if (n < g.e_lo[j] || n >= g.e_hi[j]) return;
+  const int re = tab[a].re;
+  if (re > 16) return;
+  const int ldb = g.e_hi[j] - g.e_lo[j];
+  const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + tab[a].offB[j]) + (n - g.e_lo[j]);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) pre.b[q] = (q < re) ? bf16_bits_to_f32(__ldg(B + (size_t)q * ldb)) : 0.f;
+  pre.a = a;
+}
+
 __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int cnt, const int* s_ids,
                                              const int* s_lead, const SlotEntry* __restrict__ tab,
                                              const __nv_bfloat16* __restrict__ arena, const Geom& g,
-                                             const float* __restrict__ v, int T) {
+                                             const float* __restrict__ v, int T, const LoraPre* pre = nullptr) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) lr[i] = 0.f;
   if (n >= g.M) return;
@@ -137,9 +171,14 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
     for (int c = 0; c < g.C; ++c) {
       for (int k0 = 0; k0 < rc; k0 += 16) {
         float b[16];
+        if (pre && pre->a == a && c == 0 && k0 == 0) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q)
-          b[q] = (k0 + q < rc) ? bf16_bits_to_f32(__ldg(B + (size_t)(c * rc + k0 + q) * ldb)) : 0.f;
+          for (int q = 0; q < 16; ++q) b[q] = pre->b[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            b[q] = (k0 + q < rc) ? bf16_bits_to_f32(__ldg(B + (size_t)(c * rc + k0 + q) * ldb)) : 0.f;
+        }
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
           if (i2 < cnt && s_lead[i2] == i) {

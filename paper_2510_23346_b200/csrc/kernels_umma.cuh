@@ -241,6 +241,32 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         }
       }
     }
+    // ---- first segment: stage its token tile's ids and gather its B rows now (before v is needed) ----
+    int cur_nt = -1;
+    LoraPre pre;
+    pre.a = -1;
+    if (p.T <= kFuseMaxT && u_lo < u_hi) {
+      const int tile = u_lo / p.k_blocks, mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int t0 = nt * BN, tv = min(BN, p.T - t0);
+      for (int i = etid; i < tv; i += 128) s_ids[i] = s_fids[t0 + i];
+      ptx::named_bar_sync(1, 128);
+      for (int i = etid; i < tv; i += 128) {
+        const int cb = i & ~15, a = s_ids[i];
+        int lead = -1;
+        if (a >= 0) {
+          lead = i - cb;
+          for (int i2 = cb; i2 < i; ++i2)
+            if (s_ids[i2] == a) {
+              lead = i2 - cb;
+              break;
+            }
+        }
+        s_lead[i] = lead;
+      }
+      ptx::named_bar_sync(1, 128);
+      cur_nt = nt;
+      lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
+    }
     if (p.fuse) {
       // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
       // Units (leader token t, slice j, rank row k) are computed by the epilogue warps while the
@@ -321,7 +347,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
     int acc = 0;
     uint32_t acc_phase = 0;
-    int cur_nt = -1;
+    bool first_seg = true;
     for (int u = u_lo; u < u_hi;) {
       const int tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks;
@@ -335,7 +361,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       float* my_part = p.part + ((size_t)(cta * 2 + slot) * kUmmaBM + row) * BN;
       if (nt != cur_nt) {  // stage this token tile's adapter ids
         ptx::named_bar_sync(1, 128);
-        for (int i = etid; i < tv; i += 128) s_ids[i] = __ldg(p.ids + t0 + i);
+        for (int i = etid; i < tv; i += 128) s_ids[i] = (p.T <= kFuseMaxT) ? s_fids[t0 + i] : __ldg(p.ids + t0 + i);
         ptx::named_bar_sync(1, 128);
         for (int i = etid; i < tv; i += 128) {  // group leader within the token's 16-chunk
           const int cb = i & ~15, a = s_ids[i];
@@ -356,7 +382,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       // LoRA term of the first 16 tokens, gathered BEFORE waiting for the accumulator so it overlaps
       // this tile's mainloop.
       float lr[16];
-      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T);
+      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, first_seg ? &pre : nullptr);
+      first_seg = false;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       if (etid == 0) {
@@ -516,9 +543,9 @@ inline bool encode_kmajor(CUtensorMap* m, const void* base, int K, int rows, int
   return r == CUDA_SUCCESS;
 }
 
-// Ring depth.  Decode is an HBM stream: ~1 us of DRAM latency x 44 GB/s per SM needs ~3-4 stages of 18 KB;
-// deeper rings only queue more bytes in HBM, which inflates the latency of every dependent LoRA load
-// (Little's law) without adding bandwidth.  Override with BDLORA_STAGES for tuning.
+// Ring depth.  Measured (scripts/stages_sweep.sh, 8B decode layer): 2 stages 134 us, 3: 103, 4: 100,
+// 6: 95.7, 10: 95.8 -- per-SM bandwidth needs the deep ring, at the price of a longer HBM queue that
+// the dependent LoRA loads sit in.  Default: the full ring.  Override with BDLORA_STAGES for tuning.
 inline int umma_stage_cap(int T) {
   static int env = -1;
   if (env < 0) {
@@ -526,7 +553,7 @@ inline int umma_stage_cap(int T) {
     env = s ? std::max(1, atoi(s)) : 0;
   }
   if (env > 0) return env;
-  return T <= 64 ? 4 : 64;
+  return 64;
 }
 
 template <int BN>
