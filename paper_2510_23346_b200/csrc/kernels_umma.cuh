@@ -241,32 +241,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         }
       }
     }
-    // ---- first segment: stage its token tile's ids and gather its B rows now (before v is needed) ----
     int cur_nt = -1;
     LoraPre pre;
     pre.a = -1;
-    if (p.T <= kFuseMaxT && u_lo < u_hi) {
-      const int tile = u_lo / p.k_blocks, mt = tile % p.m_tiles, nt = tile / p.m_tiles;
-      const int t0 = nt * BN, tv = min(BN, p.T - t0);
-      for (int i = etid; i < tv; i += 128) s_ids[i] = s_fids[t0 + i];
-      ptx::named_bar_sync(1, 128);
-      for (int i = etid; i < tv; i += 128) {
-        const int cb = i & ~15, a = s_ids[i];
-        int lead = -1;
-        if (a >= 0) {
-          lead = i - cb;
-          for (int i2 = cb; i2 < i; ++i2)
-            if (s_ids[i2] == a) {
-              lead = i2 - cb;
-              break;
-            }
-        }
-        s_lead[i] = lead;
-      }
-      ptx::named_bar_sync(1, 128);
-      cur_nt = nt;
-      lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
-    }
     if (p.fuse) {
       // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
       // Units (leader token t, slice j, rank row k) are computed by the epilogue warps while the
@@ -337,10 +314,35 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       }
       ptx::named_bar_sync(1, 128);
       if (etid == 0 && mine) ptx::atom_add_acq_rel_gpu(p.sync + 1, mine);  // publishes my v (release)
+    }
+    // ---- first segment: stage its token tile's ids and gather its B rows now (before v is needed) ----
+    if (p.T <= kFuseMaxT && u_lo < u_hi) {
+      const int tile = u_lo / p.k_blocks, mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int t0 = nt * BN, tv = min(BN, p.T - t0);
+      for (int i = etid; i < tv; i += 128) s_ids[i] = s_fids[t0 + i];
+      ptx::named_bar_sync(1, 128);
+      for (int i = etid; i < tv; i += 128) {
+        const int cb = i & ~15, a = s_ids[i];
+        int lead = -1;
+        if (a >= 0) {
+          lead = i - cb;
+          for (int i2 = cb; i2 < i; ++i2)
+            if (s_ids[i2] == a) {
+              lead = i2 - cb;
+              break;
+            }
+        }
+        s_lead[i] = lead;
+      }
+      ptx::named_bar_sync(1, 128);
+      cur_nt = nt;
+      lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
+    }
+    if (p.fuse) {
       // every unit of the launch published before any expand reads v
       if (etid == 0) {
         UMMA_TRACE(13);
-        while (ptx::ld_acquire_gpu(p.sync + 1) < U_s) __nanosleep(64);
+        while (ptx::ld_acquire_gpu(p.sync + 1) < p.T * p.g.J * p.rs_max) __nanosleep(64);
         UMMA_TRACE(14);
       }
       ptx::named_bar_sync(1, 128);
