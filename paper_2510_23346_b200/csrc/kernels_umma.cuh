@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       // this tile's mainloop.
       float lr[16];
       lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, first_seg ? &pre : nullptr);
+      if (first_seg && etid == 0) UMMA_TRACE(15);
       first_seg = false;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();

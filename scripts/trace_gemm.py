@@ -44,7 +44,7 @@ used = t[:, 0] > 0
 t = t[used]
 t0 = t[:, 0].min()
 names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit", "fin_beg",
-         "fin_end", "arrived", "part_beg", "shr_done", "v_ready"]
+         "fin_end", "arrived", "part_beg", "shr_done", "v_ready", "lora1"]
 print(f"M={M} K={K} T={T} event time {s.elapsed_time(e)*1e3:.1f} us, CTAs {used.sum()}")
 for k, nm in enumerate(names):
     col = (t[:, k] - t0) / 1e3
