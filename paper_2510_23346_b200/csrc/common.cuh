@@ -185,7 +185,7 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
             const float* vv = v + ((size_t)(c * T + tb + i2) * g.J + j) * g.Rc + k0;
             float vk[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? __ldcg(vv + q) : 0.f;  // coherent: v may be written in-kernel
+            for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? __ldg(vv + q) : 0.f;  // L1 broadcast (v never read before it is final)
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
             for (int q = 0; q < 16; q += 4) {
