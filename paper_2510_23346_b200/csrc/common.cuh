@@ -152,9 +152,23 @@ __device__ __forceinline__ void lora_pre16(LoraPre& pre, int n, int cnt, const i
 __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int cnt, const int* s_ids,
                                              const int* s_lead, const SlotEntry* __restrict__ tab,
                                              const __nv_bfloat16* __restrict__ arena, const Geom& g,
-                                             const float* __restrict__ v, int T, const LoraPre* pre = nullptr) {
+                                             const float* __restrict__ v, int T, const LoraPre* pre = nullptr,
+                                             float* s_v = nullptr, int s_v_cap = 0, int etid = 0) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) lr[i] = 0.f;
+  // Stage this chunk's v rows in shared memory (cooperatively, once) when they fit: the inner loop then
+  // reads them with broadcast LDS instead of one global load per (token, rank) per thread.
+  const int per_tok = g.J * g.Rc;
+  const bool staged = s_v != nullptr && g.C * 16 * per_tok <= s_v_cap;
+  if (staged) {
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // previous readers of s_v are done
+    for (int c = 0; c < g.C; ++c) {
+      const float* src = v + (size_t)(c * T + tb) * per_tok;
+      float* dst = s_v + (size_t)c * 16 * per_tok;
+      for (int idx = etid; idx < cnt * per_tok; idx += 128) dst[idx] = __ldg(src + idx);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+  }
   if (n >= g.M) return;
   int j = 0;
 #pragma unroll
@@ -182,10 +196,27 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
           if (i2 < cnt && s_lead[i2] == i) {
-            const float* vv = v + ((size_t)(c * T + tb + i2) * g.J + j) * g.Rc + k0;
             float vk[16];
+            if (staged) {
+              const float* vv = s_v + ((size_t)(c * 16 + i2) * g.J + j) * g.Rc + k0;
+              if ((g.Rc & 3) == 0 && k0 + 16 <= rc) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? __ldg(vv + q) : 0.f;  // L1 broadcast (v never read before it is final)
+                for (int q = 0; q < 16; q += 4) {
+                  const float4 f4 = *reinterpret_cast<const float4*>(vv + q);
+                  vk[q] = f4.x;
+                  vk[q + 1] = f4.y;
+                  vk[q + 2] = f4.z;
+                  vk[q + 3] = f4.w;
+                }
+              } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? vv[q] : 0.f;
+              }
+            } else {
+              const float* vv = v + ((size_t)(c * T + tb + i2) * g.J + j) * g.Rc + k0;
+#pragma unroll
+              for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? __ldg(vv + q) : 0.f;  // L1 broadcast
+            }
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
             for (int q = 0; q < 16; q += 4) {

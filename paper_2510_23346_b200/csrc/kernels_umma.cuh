@@ -77,7 +77,9 @@ struct UmmaSmem {
   static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kBytes = kBarOff + 256 + 4096 + 128 + 1024;  // + barriers/flags, ids/leaders/shrink, slack
+  static constexpr int kVOff = kBarOff + 256 + 4096 + 128;          // after barriers/flags, ids/leaders/shrink
+  static constexpr int kVFloats = 4096;                              // 16 KB v staging
+  static constexpr int kBytes = kVOff + kVFloats * 4 + 1024;         // + alignment slack
 };
 
 template <int BN>
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_mem = s_fids + 256;                     // [T] members of the current adapter group
   float* s_red = (float*)(s_mem + 256);          // [4][4] cross-warp partial dots
   int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count
+  float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -384,7 +387,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       // LoRA term of the first 16 tokens, gathered BEFORE waiting for the accumulator so it overlaps
       // this tile's mainloop.
       float lr[16];
-      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, first_seg ? &pre : nullptr);
+      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, first_seg ? &pre : nullptr,
+                   s_v, S::kVFloats, etid);
       if (first_seg && etid == 0) UMMA_TRACE(15);
       first_seg = false;
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -399,7 +403,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::tmem_ld_32x32b_x16(taddr + c0, r);
         ptx::tmem_ld_wait();
         if (whole) {
-          if (c0 > 0) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T);
+          if (c0 > 0)
+            lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T,
+                         nullptr, s_v, S::kVFloats, etid);
           if (n < p.M) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -437,7 +443,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           const int c_first = umma_cta_of(ts, p.units, p.grid);
           const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
           for (int c0 = 0; c0 < tv; c0 += 16) {
-            if (c0 > 0 || tv > 16) lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T);
+            if (c0 > 0 || tv > 16)
+              lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v,
+                           p.T, nullptr, s_v, S::kVFloats, etid);
             const int nq = min(4, (tv - c0 + 3) / 4);  // float4 groups holding valid tokens
             float y[16];
 #pragma unroll
