@@ -77,7 +77,7 @@ struct UmmaSmem {
   static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kVOff = kBarOff + 256 + 4096 + 128;          // after barriers/flags, ids/leaders/shrink
+  static constexpr int kVOff = kBarOff + 256 + 5120 + 128;          // after barriers/flags, ids/leaders/shrink
   static constexpr int kVFloats = 4096;                              // 16 KB v staging
   static constexpr int kBytes = kVOff + kVFloats * 4 + 1024;         // + alignment slack
 };
@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_lead = s_ids + 256;                     // [BN] group leader of each token in its 16-chunk
   int* s_fids = s_lead + 256;                    // [T <= 256] all ids (fused shrink)
   int* s_mem = s_fids + 256;                     // [T] members of the current adapter group
-  float* s_red = (float*)(s_mem + 256);          // [4][4] cross-warp partial dots
+  int* s_isl = s_mem + 256;                      // [T] 1 if the token is the first of its adapter id
+  float* s_red = (float*)(s_isl + 256);          // [4][4] cross-warp partial dots
   int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
 
@@ -223,14 +224,18 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       // start of the weight stream, so the shrink's A rows and the expand's B rows hit L2 later ----------
       for (int t = etid; t < p.T; t += 128) s_fids[t] = __ldg(p.ids + t);
       ptx::named_bar_sync(1, 128);
+      for (int t = etid; t < p.T; t += 128) {  // leader = first token of its adapter id (parallel, O(T^2/128))
+        const int a = s_fids[t];
+        bool f = a >= 0;
+        for (int t2 = 0; t2 < t && f; ++t2) f = (s_fids[t2] != a);
+        s_isl[t] = f ? 1 : 0;
+      }
+      ptx::named_bar_sync(1, 128);
       const int mt_a = (u_lo / p.k_blocks) % p.m_tiles;
       const int mt_b = ((u_hi - 1) / p.k_blocks) % p.m_tiles;
       for (int t = 0; t < p.T; ++t) {  // uniform loop over distinct adapters (leaders)
+        if (!s_isl[t]) continue;
         const int a = s_fids[t];
-        if (a < 0) continue;
-        bool leader = true;
-        for (int t2 = 0; t2 < t && leader; ++t2) leader = (s_fids[t2] != a);
-        if (!leader) continue;
         const SlotEntry* e = p.tab + a;
         for (int mt = mt_a; mt <= mt_b; ++mt) {  // B rows of my output columns
           const int n0 = mt * kUmmaBM;
@@ -264,8 +269,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ++mine;
         const int t_lead = us / (Js * rsm), j = (us / rsm) % Js, k = us % rsm;
         const int a = s_fids[t_lead];
-        bool leader = a >= 0;
-        for (int t2 = 0; t2 < t_lead && leader; ++t2) leader = (s_fids[t2] != a);
+        const bool leader = s_isl[t_lead] != 0;
         const SlotEntry* e = leader ? p.tab + a : nullptr;
         if (leader && k < e->rs) {
           if (warp_e == 0) {  // members of this adapter group, token order
