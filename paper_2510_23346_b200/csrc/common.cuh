@@ -177,9 +177,14 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
   if (n < g.e_lo[j] || n >= g.e_hi[j]) return;
   const int ldb = g.e_hi[j] - g.e_lo[j];
   const int col = n - g.e_lo[j];
+  const unsigned full = (cnt >= 16) ? 0xffffu : ((1u << cnt) - 1u);
   for (int i = 0; i < cnt; ++i) {
     if (s_lead[i] != i) continue;  // not a group leader (or no adapter)
     const int a = s_ids[i];
+    unsigned mask = 0;              // members of this group within the chunk (warp-uniform)
+#pragma unroll
+    for (int i2 = 0; i2 < 16; ++i2)
+      if (i2 < cnt && s_lead[i2] == i) mask |= 1u << i2;
     const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + tab[a].offB[j]) + col;
     const int rc = tab[a].re / g.C;
     for (int c = 0; c < g.C; ++c) {
@@ -193,25 +198,43 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
           for (int q = 0; q < 16; ++q)
             b[q] = (k0 + q < rc) ? bf16_bits_to_f32(__ldg(B + (size_t)(c * rc + k0 + q) * ldb)) : 0.f;
         }
+        const bool vec = staged && (g.Rc & 3) == 0 && k0 + 16 <= rc;
+        if (vec && mask == full) {
+          // one adapter for the whole chunk: branch-free, every LDS.128 independent (pipelined)
+#pragma unroll
+          for (int i2 = 0; i2 < 16; ++i2) {
+            const float* vv = s_v + ((size_t)(c * 16 + i2) * g.J + j) * g.Rc + k0;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+              const float4 f4 = *reinterpret_cast<const float4*>(vv + q);
+              s0 = fmaf(f4.x, b[q], s0);
+              s1 = fmaf(f4.y, b[q + 1], s1);
+              s2 = fmaf(f4.z, b[q + 2], s2);
+              s3 = fmaf(f4.w, b[q + 3], s3);
+            }
+            if (i2 < cnt) lr[i2] += (s0 + s1) + (s2 + s3);
+          }
+          continue;
+        }
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
-          if (i2 < cnt && s_lead[i2] == i) {
+          if ((mask >> i2) & 1u) {
             float vk[16];
-            if (staged) {
+            if (vec) {
               const float* vv = s_v + ((size_t)(c * 16 + i2) * g.J + j) * g.Rc + k0;
-              if ((g.Rc & 3) == 0 && k0 + 16 <= rc) {
 #pragma unroll
-                for (int q = 0; q < 16; q += 4) {
-                  const float4 f4 = *reinterpret_cast<const float4*>(vv + q);
-                  vk[q] = f4.x;
-                  vk[q + 1] = f4.y;
-                  vk[q + 2] = f4.z;
-                  vk[q + 3] = f4.w;
-                }
-              } else {
-#pragma unroll
-                for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? vv[q] : 0.f;
+              for (int q = 0; q < 16; q += 4) {
+                const float4 f4 = *reinterpret_cast<const float4*>(vv + q);
+                vk[q] = f4.x;
+                vk[q + 1] = f4.y;
+                vk[q + 2] = f4.z;
+                vk[q + 3] = f4.w;
               }
+            } else if (staged) {
+              const float* vv = s_v + ((size_t)(c * 16 + i2) * g.J + j) * g.Rc + k0;
+#pragma unroll
+              for (int q = 0; q < 16; ++q) vk[q] = (k0 + q < rc) ? vv[q] : 0.f;
             } else {
               const float* vv = v + ((size_t)(c * T + tb + i2) * g.J + j) * g.Rc + k0;
 #pragma unroll
