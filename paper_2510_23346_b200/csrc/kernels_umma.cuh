@@ -19,6 +19,7 @@
 // dependent launch the W stream of this kernel overlaps it and only the epilogue waits for it.
 #pragma once
 #include "common.cuh"
+#include "kernels_route.cuh"
 #include "ptx.cuh"
 
 #include <algorithm>
@@ -48,7 +49,8 @@ struct UmmaParams {
   int pdl;
   int nstages;       // ring stages actually used (<= kStages): bounds the bytes in flight per SM
   int fuse;          // 1: the epilogue warps also compute v (fused shrink); 0: v comes from a prior kernel
-  float* v_out;      // fused mode: v [T][J][Rc] written here (== v)
+  float* v_out;      // fused mode / shrink mode: v [T][J][Rc] written here
+  const int* route;  // shrink mode: groups + 16-row A boxes from route_kernel (RouteLayout)
   int* sync;         // fused mode: [0] unit claim counter, [1] units done, [2] CTAs exited (zero between launches)
   long long* trace;  // optional per-CTA timestamps (ns, %globaltimer) for profiling; nullptr = off
 };
@@ -82,7 +84,7 @@ struct UmmaSmem {
   static constexpr int kBytes = kVOff + kVFloats * 4 + 1024;         // + alignment slack
 };
 
-template <int BN>
+template <int BN, int MODE>
 __global__ void __launch_bounds__(kUmmaThreads, 1)
     umma_lora_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                           const UmmaParams p) {
@@ -108,8 +110,19 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
-  const int u_lo = umma_u_lo(cta, p.units, p.grid);
-  const int u_hi = umma_u_lo(cta + 1, p.units, p.grid);
+  // MODE 0: base GEMM (+ fused shrink / LoRA expand epilogue).  MODE 1: tensor-core shrink -- the
+  // "weight" rows are 16-row boxes of adapter A rows listed by route_kernel, the output is v (fp32).
+  int M_TILES = M_TILES, UNITS = UNITS, GRID = GRID, n_items = 0;
+  if constexpr (MODE == 1) {
+    ptx::pdl_wait();  // the route kernel (preceding) produced the item list
+    n_items = p.route[RouteLayout::kHdr + 1];
+    M_TILES = (n_items + 7) / 8;
+    UNITS = M_TILES * p.n_tiles * p.k_blocks;
+    GRID = max(1, min((int)gridDim.x, UNITS / 8));
+  }
+  const bool active = cta < GRID && UNITS > 0;
+  const int u_lo = active ? umma_u_lo(cta, UNITS, GRID) : 0;
+  const int u_hi = active ? umma_u_lo(cta + 1, UNITS, GRID) : 0;
   if (threadIdx.x == 0) UMMA_TRACE(0);
 
   if (warp == 0 && lane == 0) {
@@ -142,28 +155,57 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     // ------------------------------------------------------------ TMA producer
     // Weights never depend on the preceding kernel: the first ring of W tiles is issued BEFORE the
     // programmatic-dependency wait (overlapping the previous kernel's tail), activations after it.
-    if (ptx::elect_one()) {
+    if (MODE == 1 && ptx::elect_one()) {
+      // shrink: up to 8 boxes of 16 A rows per 128-row tile (rows of different adapters / slices)
+      const uint64_t pol_a = ptx::policy_evict_first();
+      const uint64_t pol_x = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int cur_mt = -1, nbox = 0;
+      int rows[8];
+      for (int u = u_lo; u < u_hi; ++u) {
+        const int tile = u / p.k_blocks, kb = u - tile * p.k_blocks;
+        const int mt = tile % M_TILES, nt = tile / M_TILES;
+        if (mt != cur_mt) {
+          cur_mt = mt;
+          nbox = min(8, n_items - mt * 8);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) rows[b] = (b < nbox) ? p.route[RouteLayout::kItemRow + mt * 8 + b] : 0;
+        }
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[stage], nbox * 2048 + S::kXBytes);
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (b < nbox)
+            ptx::tma_load_2d(sW + stage * S::kWBytes + b * 2048, &tmW, &full[stage], kb * kUmmaBK, rows[b], pol_a);
+        ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
+        if (++stage == p.nstages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else if (MODE == 0 && ptx::elect_one()) {
       const uint64_t pol_w = ptx::policy_evict_first();
       const uint64_t pol_x = ptx::policy_evict_last();
       const int nu = u_hi - u_lo;
       const int NS = p.nstages;
       const int P = min(nu, NS);
       for (int idx = 0; idx < P; ++idx) {
-        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, mt = tile % p.m_tiles;
+        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, mt = tile % M_TILES;
         ptx::mbar_arrive_expect_tx(&full[idx], S::kStageBytes);
         ptx::tma_load_2d(sW + idx * S::kWBytes, &tmW, &full[idx], kb * kUmmaBK, mt * kUmmaBM, pol_w);
       }
       if (nu > 0) UMMA_TRACE(2);
       if (p.pdl) ptx::pdl_wait();
       for (int idx = 0; idx < P; ++idx) {
-        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, nt = tile / p.m_tiles;
+        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, nt = tile / M_TILES;
         ptx::tma_load_2d(sX + idx * S::kXBytes, &tmX, &full[idx], kb * kUmmaBK, nt * BN, pol_x);
       }
       int stage = (P == NS) ? 0 : P;
       uint32_t phase = (P == NS) ? 1u : 0u;
       for (int idx = P; idx < nu; ++idx) {
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks;
-        const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+        const int mt = tile % M_TILES, nt = tile / M_TILES;
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
         ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
@@ -213,6 +255,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
+    if constexpr (MODE == 0) {
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..127
@@ -231,8 +274,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         s_isl[t] = f ? 1 : 0;
       }
       ptx::named_bar_sync(1, 128);
-      const int mt_a = (u_lo / p.k_blocks) % p.m_tiles;
-      const int mt_b = ((u_hi - 1) / p.k_blocks) % p.m_tiles;
+      const int mt_a = (u_lo / p.k_blocks) % M_TILES;
+      const int mt_b = ((u_hi - 1) / p.k_blocks) % M_TILES;
       for (int t = 0; t < p.T; ++t) {  // uniform loop over distinct adapters (leaders)
         if (!s_isl[t]) continue;
         const int a = s_fids[t];
@@ -324,7 +367,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
     // ---- first segment: stage its token tile's ids and gather its B rows now (before v is needed) ----
     if (p.T <= kFuseMaxT && u_lo < u_hi) {
-      const int tile = u_lo / p.k_blocks, mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int tile = u_lo / p.k_blocks, mt = tile % M_TILES, nt = tile / M_TILES;
       const int t0 = nt * BN, tv = min(BN, p.T - t0);
       for (int i = etid; i < tv; i += 128) s_ids[i] = s_fids[t0 + i];
       ptx::named_bar_sync(1, 128);
@@ -361,7 +404,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const int tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks;
       const int kb1 = min(p.k_blocks, kb0 + (u_hi - u));
-      const int mt = tile % p.m_tiles, nt = tile / p.m_tiles;
+      const int mt = tile % M_TILES, nt = tile / M_TILES;
       const int n = mt * kUmmaBM + row;
       const int t0 = nt * BN;
       const int tv = min(BN, p.T - t0);
@@ -444,8 +487,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           // loads in flight per round, add the LoRA term, round once, store.
           if (etid == 0) UMMA_TRACE(9);
           const int ts = tile * p.k_blocks;
-          const int c_first = umma_cta_of(ts, p.units, p.grid);
-          const int c_last = umma_cta_of(ts + p.k_blocks - 1, p.units, p.grid);
+          const int c_first = umma_cta_of(ts, UNITS, GRID);
+          const int c_last = umma_cta_of(ts + p.k_blocks - 1, UNITS, GRID);
           for (int c0 = 0; c0 < tv; c0 += 16) {
             if (c0 > 0 || tv > 16)
               lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v,
@@ -459,7 +502,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
 #pragma unroll
               for (int cc = 0; cc < 8; ++cc) {
                 const int c = cb + cc;
-                const int sl = (c <= c_last && ts > umma_u_lo(c, p.units, p.grid)) ? 1 : 0;
+                const int sl = (c <= c_last && ts > umma_u_lo(c, UNITS, GRID)) ? 1 : 0;
                 const float4* src = reinterpret_cast<const float4*>(
                     p.part + ((size_t)(min(c, c_last) * 2 + sl) * kUmmaBM + row) * BN + c0);
 #pragma unroll
@@ -494,7 +537,121 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       u += kb1 - kb0;
       if (etid == 0) UMMA_TRACE(7);
     }
+    } else {
+      // ------------------------------------------------ shrink epilogue: v = s_a * acc, member tokens only
+      const int q = warp & 3;
+      const int row = q * 32 + lane;
+      const int etid = threadIdx.x - 64;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      int cur_nt = -1;
+      for (int u = u_lo; u < u_hi;) {
+        const int tile = u / p.k_blocks;
+        const int kb0 = u - tile * p.k_blocks;
+        const int kb1 = min(p.k_blocks, kb0 + (u_hi - u));
+        const int mt = tile % M_TILES, nt = tile / M_TILES;
+        const int t0 = nt * BN;
+        const int tv = min(BN, p.T - t0);
+        const bool whole = (kb0 == 0 && kb1 == p.k_blocks);
+        const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
+        float* my_part = p.part + ((size_t)(cta * 2 + slot) * kUmmaBM + row) * BN;
+        if (nt != cur_nt) {
+          ptx::named_bar_sync(1, 128);
+          for (int i = etid; i < tv; i += 128) s_ids[i] = __ldg(p.ids + t0 + i);
+          ptx::named_bar_sync(1, 128);
+          cur_nt = nt;
+        }
+        // this thread's accumulator row -> (adapter, slice, rank row) of the box it belongs to
+        const int item = mt * 8 + (row >> 4), rr = row & 15;
+        int va = -2, vj = 0, vk = 0;
+        float vsc = 0.f;
+        if (item < n_items && rr < p.route[RouteLayout::kItemN + item]) {
+          va = p.route[RouteLayout::kGroupId + p.route[RouteLayout::kItemG + item]];
+          vj = p.route[RouteLayout::kItemJ + item];
+          vk = p.route[RouteLayout::kItemK0 + item] + rr;
+          vsc = p.tab[va].scale;
+        }
+        ptx::mbar_wait(&tfull[acc], acc_phase);
+        ptx::tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+        for (int c0 = 0; c0 < tv; c0 += 16) {
+          uint32_t r[16];
+          ptx::tmem_ld_32x32b_x16(taddr + c0, r);
+          ptx::tmem_ld_wait();
+          if (whole) {
+            if (va >= 0) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (c0 + i < tv && s_ids[c0 + i] == va)
+                  p.v_out[((size_t)(t0 + c0 + i) * p.g.J + vj) * p.g.Rc + vk] = vsc * __uint_as_float(r[i]);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              __stcg(reinterpret_cast<float4*>(my_part + c0 + i),
+                     make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+                                 __uint_as_float(r[i + 3])));
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+        if (!whole) {
+          ptx::named_bar_sync(1, 128);
+          if (etid == 0) {
+            const int got = kb1 - kb0;
+            const int old = ptx::atom_add_acq_rel_gpu(p.tile_cnt + tile, got);
+            *s_last = (old + got == p.k_blocks);
+          }
+          ptx::named_bar_sync(1, 128);
+          if (*s_last) {
+            const int ts = tile * p.k_blocks;
+            const int c_first = umma_cta_of(ts, UNITS, GRID);
+            const int c_last = umma_cta_of(ts + p.k_blocks - 1, UNITS, GRID);
+            for (int c0 = 0; c0 < tv; c0 += 16) {
+              const int nq = min(4, (tv - c0 + 3) / 4);
+              float y[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) y[i] = 0.f;
+              for (int cb = c_first; cb <= c_last; cb += 8) {
+                float4 buf[8][4];
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                  const int c = cb + cc;
+                  const int sl = (c <= c_last && ts > umma_u_lo(c, UNITS, GRID)) ? 1 : 0;
+                  const float4* src = reinterpret_cast<const float4*>(
+                      p.part + ((size_t)(min(c, c_last) * 2 + sl) * kUmmaBM + row) * BN + c0);
+#pragma unroll
+                  for (int g4 = 0; g4 < 4; ++g4)
+                    buf[cc][g4] = (c <= c_last && g4 < nq) ? __ldcg(src + g4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc)
+#pragma unroll
+                  for (int g4 = 0; g4 < 4; ++g4) {
+                    y[4 * g4] += buf[cc][g4].x;
+                    y[4 * g4 + 1] += buf[cc][g4].y;
+                    y[4 * g4 + 2] += buf[cc][g4].z;
+                    y[4 * g4 + 3] += buf[cc][g4].w;
+                  }
+              }
+              if (va >= 0) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                  if (c0 + i < tv && s_ids[c0 + i] == va)
+                    p.v_out[((size_t)(t0 + c0 + i) * p.g.J + vj) * p.g.Rc + vk] = vsc * y[i];
+              }
+            }
+            if (etid == 0) p.tile_cnt[tile] = 0;
+          }
+          ptx::named_bar_sync(1, 128);
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        u += kb1 - kb0;
+      }
+    }
   }
+
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -571,21 +728,18 @@ inline int umma_stage_cap(int T) {
   return 64;
 }
 
-template <int BN>
-inline int umma_launch_bn(const UmmaParams& p0, const __nv_bfloat16* X, const __nv_bfloat16* W, cudaStream_t st) {
+template <int BN, int MODE>
+inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CUtensorMap& tmX, cudaStream_t st) {
   using S = UmmaSmem<BN>;
   UmmaParams p1 = p0;
   p1.nstages = std::min(S::kStages, umma_stage_cap(p0.T));
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             S::kBytes) != cudaSuccess)
       return 2;
     attr_set = true;
   }
-  CUtensorMap tmW, tmX;
-  if (!encode_kmajor(&tmW, W, p0.K, p0.M, kUmmaBM)) return 3;
-  if (!encode_kmajor(&tmX, X, p0.K, p0.T, BN)) return 3;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p0.grid);
   cfg.blockDim = dim3(kUmmaThreads);
@@ -596,8 +750,20 @@ inline int umma_launch_bn(const UmmaParams& p0, const __nv_bfloat16* X, const __
   attr[0].val.programmaticStreamSerializationAllowed = p0.pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN>, tmW, tmX, p1) != cudaSuccess) return 4;
+  if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN, MODE>, tmW, tmX, p1) != cudaSuccess) return 4;
   return 0;
+}
+
+template <int MODE>
+inline int umma_dispatch_bn(int BN, const UmmaParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                            cudaStream_t st) {
+  switch (BN) {
+    case 16: return umma_launch_bn<16, MODE>(p, tmW, tmX, st);
+    case 32: return umma_launch_bn<32, MODE>(p, tmW, tmX, st);
+    case 64: return umma_launch_bn<64, MODE>(p, tmW, tmX, st);
+    case 128: return umma_launch_bn<128, MODE>(p, tmW, tmX, st);
+    default: return umma_launch_bn<256, MODE>(p, tmW, tmX, st);
+  }
 }
 
 // Returns 0 on launch, non-zero if the shape is not handled here.
@@ -645,14 +811,55 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   if (v_fused) p.v = v_fused;
   p.pdl = pdl;
   p.trace = g_umma_trace;
-  p.nstages = 0;  // set per BN below
-  switch (BN) {
-    case 16: return umma_launch_bn<16>(p, X, W, st);
-    case 32: return umma_launch_bn<32>(p, X, W, st);
-    case 64: return umma_launch_bn<64>(p, X, W, st);
-    case 128: return umma_launch_bn<128>(p, X, W, st);
-    default: return umma_launch_bn<256>(p, X, W, st);
-  }
+  p.nstages = 0;  // set per BN
+  p.route = nullptr;
+  CUtensorMap tmW, tmX;
+  if (!encode_kmajor(&tmW, W, p.K, p.M, kUmmaBM)) return 3;
+  if (!encode_kmajor(&tmX, X, p.K, p.T, BN)) return 3;
+  return umma_dispatch_bn<0>(BN, p, tmW, tmX, st);
+}
+
+// Tensor-core shrink: v[t][j][k] = s_a X[t] . A_{a,j}[k] for every token t of every distinct adapter a,
+// the A rows gathered in 16-row TMA boxes through `amap` (the pool arena viewed as [rows, K]).  The item
+// list comes from route_kernel (launched just before).  Workspace as umma_workspace_bytes(items_max*16, T).
+inline size_t umma_shrink_workspace_bytes(int items_max, int T, int num_sms = 148) {
+  return umma_workspace_bytes(((items_max + 7) / 8) * kUmmaBM, T, num_sms);
+}
+
+inline int umma_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* ids, const SlotEntry* tab,
+                              const int* route, const CUtensorMap& amap, float* v_out, int items_max, void* ws,
+                              int num_sms, cudaStream_t st, int pdl) {
+  if (g.K % kUmmaBK != 0 || T < 1) return 1;
+  const int BN = umma_bn_for(T);
+  UmmaParams p{};
+  p.M = 0;
+  p.K = g.K;
+  p.T = T;
+  p.m_tiles = (items_max + 7) / 8;
+  p.n_tiles = (T + BN - 1) / BN;
+  p.k_blocks = g.K / kUmmaBK;
+  const long long units_max = (long long)p.m_tiles * p.n_tiles * p.k_blocks;
+  if (units_max > (1LL << 30)) return 1;
+  p.units = (int)units_max;
+  p.grid = (int)std::max<long long>(1, std::min<long long>(units_max / 8, num_sms));
+  p.ids = ids;
+  p.tab = tab;
+  p.g = g;
+  p.v = nullptr;
+  p.Y = nullptr;
+  const size_t cnt_bytes = (((size_t)p.m_tiles * p.n_tiles * sizeof(int)) + 255) / 256 * 256;
+  p.sync = (int*)ws;
+  p.tile_cnt = (int*)((char*)ws + 256);
+  p.part = (float*)((char*)ws + 256 + cnt_bytes);
+  p.X = X;
+  p.fuse = 0;
+  p.v_out = v_out;
+  p.route = route;
+  p.pdl = pdl;
+  p.trace = nullptr;
+  CUtensorMap tmX;
+  if (!encode_kmajor(&tmX, X, p.K, p.T, BN)) return 3;
+  return umma_dispatch_bn<1>(BN, p, amap, tmX, st);
 }
 
 }  // namespace bdl

@@ -97,6 +97,8 @@ struct bdlora_pool {
   bool ragged = false;
   int64_t resident_elems = 0;
   int num_sms = 148;
+  CUtensorMap amap;      // the arena as a [arena_elems / K, K] bf16 tensor, 16-row boxes (tensor-core shrink)
+  bool amap_ok = false;
 };
 
 namespace {
@@ -117,7 +119,10 @@ int64_t slot_elems_for_rank(const bdlora_pool* p, int r) {
   }
   int64_t e = 0;
   for (int j = 0; j < p->g.J; ++j) e += (int64_t)rs * p->g.K + (int64_t)re * p->ldb[j];
-  return e;
+  // slot regions are whole rows of K elements: every A row starts at a multiple of K, so one TMA
+  // tensor map over the arena ([arena_elems / K, K]) addresses any adapter's A rows (tensor-core shrink)
+  const int64_t K = p->g.K;
+  return (e + K - 1) / K * K;
 }
 
 void ranks_for(const bdlora_pool* p, int r, int* rs, int* re) {
@@ -141,8 +146,20 @@ constexpr int kMaxTiles = 8192;
 constexpr int kPartTokenSplits = 64;  // S x min(T, 8) <= 64 for the split-K GEMV
 
 struct WsLayout {
-  size_t off_counters, off_v, off_part, off_umma, total;
+  size_t off_counters, off_v, off_part, off_umma, off_route, off_shrink, total;
 };
+
+constexpr int kTcShrinkMinT = 17;  // tensor-core shrink above decode sizes (T <= 16: fused CUDA-core shrink)
+
+// Upper bound of the tensor-core shrink's 16-row A boxes for a batch of T tokens (0 = not eligible).
+int tc_items_max(const bdlora_pool* p, int64_t T) {
+  if (!p->amap_ok || p->g.K % 64 != 0 || T < kTcShrinkMinT || T > bdl::kRouteMaxSeg) return 0;
+  const int64_t groups = std::min<int64_t>(T, p->d.capacity);
+  if (groups > bdl::kRouteMaxGroups) return 0;
+  const int64_t items = groups * p->g.J * ((p->rs_max + 15) / 16);
+  if (items > bdl::kRouteMaxItems) return 0;
+  return (int)items;
+}
 
 WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   WsLayout L;
@@ -156,6 +173,11 @@ WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   o = align_up(o + sizeof(float) * (size_t)kPartTokenSplits * p->g.M, 256);
   L.off_umma = o;
   o = align_up(o + bdl::umma_workspace_bytes(p->g.M, (int)T, p->num_sms), 256);
+  L.off_route = o;
+  const int items = tc_items_max(p, T);
+  if (items > 0) o = align_up(o + sizeof(int) * bdl::RouteLayout::kWords, 256);
+  L.off_shrink = o;
+  if (items > 0) o = align_up(o + bdl::umma_shrink_workspace_bytes(items, (int)T, p->num_sms), 256);
   L.total = o;
   return L;
 }
@@ -184,8 +206,34 @@ int check_fwd_args(const bdlora_pool* p, const void* X, int64_t T, const void* W
 // ---------------------------------------------------------------------------- launches
 int g_pdl = 1;  // programmatic dependent launch chaining (bdlora_set_pdl)
 
-int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids, float* v, cudaStream_t st) {
+WsLayout ws_layout(const bdlora_pool* p, int64_t T);
+
+int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids, float* v, cudaStream_t st,
+                  void* ws = nullptr) {
   if (T == 0) return BDLORA_OK;
+  const int items = ws ? tc_items_max(p, T) : 0;
+  if (items > 0) {
+    // tensor-core shrink: route (groups + A boxes) -> grouped tcgen05 GEMM writing v
+    const WsLayout L = ws_layout(p, T);
+    int* route = (int*)((char*)ws + L.off_route);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CU_TRY(cudaLaunchKernelEx(&cfg, bdl::route_kernel, ids, T, (const SlotEntry*)p->d_tab, p->g, route));
+    count_launch();
+    int rc = bdl::umma_shrink_launch(p->g, (const __nv_bfloat16*)X, T, ids, p->d_tab, route, p->amap, v, items,
+                                     (char*)ws + L.off_shrink, p->num_sms, st, g_pdl);
+    if (rc != 0) return fail(BDLORA_E_CUDA, "tensor-core shrink launch failed (%d): %s", rc,
+                             cudaGetErrorString(cudaGetLastError()));
+    count_launch();
+    return BDLORA_OK;
+  }
   const Geom& g = p->g;
   if (T > 65535 * 16) return fail(BDLORA_E_CAPACITY, "T = %d too large for the shrink grid", T);
   cudaLaunchConfig_t cfg = {};
@@ -450,7 +498,7 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
     p->arena_elems = per_slot * d.capacity;
     p->ragged = false;
   } else {
-    p->arena_elems = d.arena_bytes / 2;
+    p->arena_elems = d.arena_bytes / 2 / g.K * g.K;
     p->ragged = true;
     p->free_list[0] = p->arena_elems;
   }
@@ -468,6 +516,8 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
   }
   cudaMemset(p->d_tab, 0, sizeof(SlotEntry) * d.capacity);
   cudaMemset(p->arena, 0, std::max<int64_t>(p->arena_elems, 8) * 2);
+  if (g.K % 64 == 0 && p->arena_elems / g.K > 0)
+    p->amap_ok = bdl::encode_kmajor(&p->amap, p->arena, g.K, (int)(p->arena_elems / g.K), 16);
   CU_TRY(cudaDeviceSynchronize());
   *out = p;
   return BDLORA_OK;
@@ -721,7 +771,8 @@ int bdlora_lora_shrink(bdlora_pool* p, const void* X, int64_t T, const int32_t* 
   (void)ws;
   (void)ws_bytes;
   DeviceGuard dg(p->dev);
-  return launch_shrink(p, X, (int)T, ids, v, (cudaStream_t)stream);
+  if (ws && ws_bytes < ws_layout(p, T).total) ws = nullptr;  // too small for the tensor-core path
+  return launch_shrink(p, X, (int)T, ids, v, (cudaStream_t)stream, ws);
 }
 
 int bdlora_base_expand(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, const float* v,
@@ -737,7 +788,7 @@ int bdlora_base_expand(bdlora_pool* p, const void* X, int64_t T, const void* W, 
 static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y, void* ws,
                     cudaStream_t st) {
   float* v = ws_v(p, ws, T);
-  if (bdl::umma_eligible(p->g, (int)T) && T <= bdl::kFuseMaxT) {
+  if (bdl::umma_eligible(p->g, (int)T) && T < kTcShrinkMinT) {
     // decode: ONE kernel -- the shrink runs in the GEMM's epilogue warps while the weights stream
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, (int)T, (const __nv_bfloat16*)W, ids, p->d_tab,
@@ -749,7 +800,7 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
       return BDLORA_OK;
     }
   }
-  ST_TRY(launch_shrink(p, X, (int)T, ids, v, st));
+  ST_TRY(launch_shrink(p, X, (int)T, ids, v, st, ws));
   // programmatic dependent launch: the GEMM streams W while the shrink runs; only its epilogue waits
   return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st);
 }
@@ -803,7 +854,7 @@ int slora_column_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64
   float* v = ws_v(p, ws, T);  // [N][T][J][Rc]
   const size_t chunk = (size_t)T * p->g.J * p->g.Rc;
   // matmul_3 into this rank's chunk, then the merged all-gather
-  ST_TRY(launch_shrink(p, X, (int)T, ids, v + chunk * p->d.tp_rank, st));
+  ST_TRY(launch_shrink(p, X, (int)T, ids, v + chunk * p->d.tp_rank, st, ws));
   if (p->d.tp_size > 1) {
     NC_TRY(ncclAllGather(v + chunk * p->d.tp_rank, v, chunk, ncclFloat32, comm->nccl, st));
     comm->counts[1] += 1;
@@ -821,7 +872,7 @@ int slora_row_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t 
   DeviceGuard dg(p->dev);
   cudaStream_t st = (cudaStream_t)stream;
   float* v = ws_v(p, ws, T);  // [T][1][Rc = max_rank]
-  ST_TRY(launch_shrink(p, X, (int)T, ids, v, st));
+  ST_TRY(launch_shrink(p, X, (int)T, ids, v, st, ws));
   if (p->d.tp_size > 1) {
     // all-reduce after matmul_5
     const size_t n = (size_t)T * p->g.Rc;
