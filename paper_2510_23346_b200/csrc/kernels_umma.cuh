@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   const int cta = blockIdx.x;
   // MODE 0: base GEMM (+ fused shrink / LoRA expand epilogue).  MODE 1: tensor-core shrink -- the
   // "weight" rows are 16-row boxes of adapter A rows listed by route_kernel, the output is v (fp32).
-  int M_TILES = M_TILES, UNITS = UNITS, GRID = GRID, n_items = 0;
+  int M_TILES = p.m_tiles, UNITS = p.units, GRID = p.grid, n_items = 0;
   if constexpr (MODE == 1) {
     ptx::pdl_wait();  // the route kernel (preceding) produced the item list
     n_items = p.route[RouteLayout::kHdr + 1];
