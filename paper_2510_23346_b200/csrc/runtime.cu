@@ -633,6 +633,8 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
     return BDLORA_OK;
   };
   int rc = BDLORA_OK;
+  // slot layout [A_0 | A_1 | A_2 | B_0 | B_1 | B_2]: every A block starts on a K-row boundary
+  int64_t curB = cur + (int64_t)J * rs * K;
   for (int j = 0; j < J && rc == BDLORA_OK; ++j) {
     const int dout = d.d_out[j];
     const int w = p->ldb[j];
@@ -666,28 +668,28 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
       // compact (r/N) x d_out_j, blocks side by side; diagonal block i = columns [i*w, ...)
       rc = src_ptr(B[j], (int64_t)(rank / N) * dout, &sb);
       if (rc) break;
-      e.offB[j] = cur;
-      rc = gather_to(sb, dout, 0, i * w, rank / N, w, 0, p->arena + cur, st);
+      e.offB[j] = curB;
+      rc = gather_to(sb, dout, 0, i * w, rank / N, w, 0, p->arena + curB, st);
     } else if (d.parallel == BDLORA_COLUMN) {
       // S-LoRA column: B_1 r x d_out_j column-sharded
       rc = src_ptr(B[j], (int64_t)rank * dout, &sb);
       if (rc) break;
-      e.offB[j] = cur;
-      rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + cur, st);
+      e.offB[j] = curB;
+      rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + curB, st);
     } else if (d.sharding == BDLORA_SHARD_BD) {
       // BD row: B_2 r x d_out row-sharded: rows [i*r/N, ...)
       rc = src_ptr(B[0], (int64_t)rank * dout, &sb);
       if (rc) break;
-      e.offB[0] = cur;
-      rc = gather_to(sb, dout, i * (rank / N), 0, rank / N, dout, 0, p->arena + cur, st);
+      e.offB[0] = curB;
+      rc = gather_to(sb, dout, i * (rank / N), 0, rank / N, dout, 0, p->arena + curB, st);
     } else {
       // S-LoRA row: B_2 r x d_out column-sharded
       rc = src_ptr(B[0], (int64_t)rank * dout, &sb);
       if (rc) break;
-      e.offB[0] = cur;
-      rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + cur, st);
+      e.offB[0] = curB;
+      rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + curB, st);
     }
-    cur += (int64_t)re * w;
+    curB += (int64_t)re * w;
   }
   if (rc != BDLORA_OK) {
     cudaStreamSynchronize(st);

@@ -516,3 +516,33 @@ def test_full_size_multitenant_70b_gate_up_tp8(dev):
                        f"70B gate_up slice {j}")
         col0 += w
     pool.close()
+
+
+@pytest.mark.parametrize("n,T,ranks", [(4, 37, [16, 16, 32]), (8, 64, [8, 24, 64, 128]), (1, 200, [16, 48])])
+def test_shrink_v_against_oracle(dev, n, T, ranks):
+    """The shrink's fp32 intermediate v (tensor-core path for T > 16, CUDA-core below) equals
+    s_a x_t A_j[:, chunk i] for every token and slice (~1e-5 relative)."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.arch_projections("llama-3.1-8b")[0]
+    case = H.make_case(950 + n + T, proj, "bd", n, T, ranks=ranks)
+    J, Rc = 3, max(ranks) // n
+    for i in (0, n - 1):
+        pool = H.make_pool(case, i)
+        X, W, ids = H.device_inputs(case, i, dev)
+        v = torch.full((bd.bdlora_v_elems(pool, T),), float("nan"), dtype=torch.float32, device=dev)
+        bd.bdlora_lora_shrink(pool, X, ids, v, bd.make_workspace(pool, T))
+        torch.cuda.synchronize()
+        vv = v.cpu().numpy().reshape(T, J, Rc).astype(np.float64)
+        for t in range(T):
+            a = int(case.ids[t])
+            if a < 0:
+                continue
+            ad = case.adapters[a]
+            rs = ad.rank // n
+            for j in range(J):
+                ref = ad.scale * (case.X.f64[t] @ ad.A[j].f64[:, i * rs:(i + 1) * rs])
+                assert np.allclose(vv[t, j, :rs], ref, rtol=1e-3, atol=1e-4 * (np.abs(ref).max() + 1)), (i, t, j)
+        pool.close()
