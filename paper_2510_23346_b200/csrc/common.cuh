@@ -152,7 +152,7 @@ __device__ __forceinline__ void lora_pre16(LoraPre& pre, int n, int cnt, const i
 __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int cnt, const int* s_ids,
                                              const int* s_lead, const SlotEntry* __restrict__ tab,
                                              const __nv_bfloat16* __restrict__ arena, const Geom& g,
-                                             const float* __restrict__ v, int T, const LoraPre* pre = nullptr,
+                                             const float* __restrict__ v, int T, LoraPre* pre = nullptr,
                                              float* s_v = nullptr, int s_v_cap = 0, int etid = 0) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) lr[i] = 0.f;
@@ -197,6 +197,11 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
 #pragma unroll
           for (int q = 0; q < 16; ++q)
             b[q] = (k0 + q < rc) ? bf16_bits_to_f32(__ldg(B + (size_t)(c * rc + k0 + q) * ldb)) : 0.f;
+          if (pre && g.C == 1 && rc <= 16) {  // keep for the next chunk of the same tile (same adapter)
+            pre->a = a;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pre->b[q] = b[q];
+          }
         }
         const bool vec = staged && (g.Rc & 3) == 0 && k0 + 16 <= rc;
         if (vec && mask == full) {

@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     bool first_seg = true;
+    int pre_n = -1;
     for (int u = u_lo; u < u_hi;) {
       const int tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks;
@@ -434,8 +435,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       // LoRA term of the first 16 tokens, gathered BEFORE waiting for the accumulator so it overlaps
       // this tile's mainloop.
       float lr[16];
-      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, first_seg ? &pre : nullptr,
-                   s_v, S::kVFloats, etid);
+      if (!first_seg && n != pre_n) pre.a = -1;  // cached B rows belong to another output column
+      pre_n = n;
+      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, &pre, s_v, S::kVFloats,
+                   etid);
       if (first_seg && etid == 0) UMMA_TRACE(15);
       first_seg = false;
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         if (whole) {
           if (c0 > 0)
             lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T,
-                         nullptr, s_v, S::kVFloats, etid);
+                         &pre, s_v, S::kVFloats, etid);
           if (n < p.M) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           for (int c0 = 0; c0 < tv; c0 += 16) {
             if (c0 > 0 || tv > 16)
               lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v,
-                           p.T, nullptr, s_v, S::kVFloats, etid);
+                           p.T, &pre, s_v, S::kVFloats, etid);
             const int nq = min(4, (tv - c0 + 3) / 4);  // float4 groups holding valid tokens
             float y[16];
 #pragma unroll
@@ -791,6 +794,10 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   if (tiles <= num_sms) {
     long long s = std::max<long long>(1, std::min<long long>(num_sms / tiles, p.k_blocks / 8));
     p.grid = (int)(tiles * s);
+  } else if (BN >= 128) {
+    // compute-bound token tiles (prefill): one whole tile per CTA, no split fix-ups (a split 128 x 256
+    // tile would move 128 KB of partials and redo the LoRA expand in the finisher)
+    p.grid = (int)tiles;
   } else {
     p.grid = (int)std::max<long long>(1, std::min<long long>(units / 8, num_sms));
   }
@@ -856,7 +863,7 @@ inline int umma_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, cons
   p.v_out = v_out;
   p.route = route;
   p.pdl = pdl;
-  p.trace = nullptr;
+  p.trace = g_umma_trace;
   CUtensorMap tmX;
   if (!encode_kmajor(&tmX, X, p.K, p.T, BN)) return 3;
   return umma_dispatch_bn<1>(BN, p, amap, tmX, st);

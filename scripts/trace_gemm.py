@@ -29,11 +29,14 @@ for i in range(6):
     bd.bdlora_base_expand(pool, X, Ws[i % nrep], ids, v, Y, ws)
 torch.cuda.synchronize()
 fused = len(sys.argv) > 4 and sys.argv[4] == "fused"
+shrink_only = len(sys.argv) > 4 and sys.argv[4] == "shrink"
 bd.bdlora_debug_trace(tr)
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s.record()
 if fused:
     bd.bdlora_column_forward(pool, X, Ws[0], ids, Y, ws)
+elif shrink_only:
+    bd.bdlora_lora_shrink(pool, X, ids, v, ws)
 else:
     bd.bdlora_base_expand(pool, X, Ws[0], ids, v, Y, ws)
 e.record()
