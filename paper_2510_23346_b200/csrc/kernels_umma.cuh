@@ -49,6 +49,7 @@ struct UmmaParams {
   int pdl;
   int nstages;       // ring stages actually used (<= kStages): bounds the bytes in flight per SM
   int fuse;          // 1: the epilogue warps also compute v (fused shrink); 0: v comes from a prior kernel
+  int tcx;           // 1: LoRA expand on the tensor cores (v split hi/lo bf16), accumulated in TMEM
   float* v_out;      // fused mode / shrink mode: v [T][J][Rc] written here
   const int* route;  // shrink mode: groups + 16-row A boxes from route_kernel (RouteLayout)
   int* sync;         // fused mode: [0] unit claim counter, [1] units done, [2] CTAs exited (zero between launches)
@@ -76,12 +77,19 @@ struct UmmaSmem {
   static constexpr int kWBytes = kUmmaBM * kUmmaBK * 2;  // 16 KB
   static constexpr int kXBytes = BN * kUmmaBK * 2;
   static constexpr int kStageBytes = kWBytes + kXBytes;
-  static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4);
+  static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kVOff = kBarOff + 256 + 5120 + 128;          // after barriers/flags, ids/leaders/shrink
-  static constexpr int kVFloats = 4096;                              // 16 KB v staging
-  static constexpr int kBytes = kVOff + kVFloats * 4 + 1024;         // + alignment slack
+  static constexpr int kVOff = kBarOff + 256 + 5120 + 256;          // after barriers/flags, ids/leaders/shrink
+  static constexpr int kVFloats = 4096;                              // 16 KB v staging (CUDA-core expand)
+  // tensor-core expand operands (share the region with the v staging): A = B-slab^T [128 x Kp],
+  // V_hi / V_lo = bf16 split of v [BN x Kp], K-major, no-swizzle core-matrix layout
+  static constexpr int kKp = BN <= 64 ? 64 : BN <= 128 ? 32 : 16;
+  static constexpr int kLoraA = 128 * kKp * 2;
+  static constexpr int kLoraV = BN * kKp * 2;
+  static constexpr int kLoraBytes = kLoraA + 2 * kLoraV;
+  static constexpr int kRegion = kLoraBytes > kVFloats * 4 ? kLoraBytes : kVFloats * 4;
+  static constexpr int kBytes = kVOff + kRegion + 1024;              // + alignment slack
 };
 
 template <int BN, int MODE>
@@ -97,7 +105,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = (uint32_t*)(tempty + 2);
+  uint64_t* lora_full = tempty + 2;   // tensor-core expand: operands built (128 epilogue arrivals)
+  uint64_t* lora_empty = lora_full + 1;  // tensor-core expand: operand MMAs done (tcgen05.commit)
+  uint32_t* tmem_holder = (uint32_t*)(lora_empty + 1);
   int* s_last = (int*)(tmem_holder + 1);
   int* s_ids = (int*)(smem + S::kBarOff + 256);  // [BN] adapter ids of the current token tile
   int* s_lead = s_ids + 256;                     // [BN] group leader of each token in its 16-chunk
@@ -105,7 +115,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_mem = s_fids + 256;                     // [T] members of the current adapter group
   int* s_isl = s_mem + 256;                      // [T] 1 if the token is the first of its adapter id
   float* s_red = (float*)(s_isl + 256);          // [4][4] cross-warp partial dots
-  int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count
+  int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count, [2] pass K, [3] last
+  int* s_pcol = s_misc + 16;                     // [8][3] tensor-core expand pass columns (a, j, k base)
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -136,6 +147,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
+    ptx::mbar_init(lora_full, 128);
+    ptx::mbar_init(lora_empty, 1);
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
@@ -224,6 +237,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      uint32_t lf_phase = 0;
       for (int u = u_lo; u < u_hi;) {
         const int tile = u / p.k_blocks;
         const int kb0 = u - tile * p.k_blocks;
@@ -244,6 +258,25 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           if (++stage == p.nstages) {
             stage = 0;
             phase ^= 1;
+          }
+        }
+        if (MODE == 0 && p.tcx && kb1 == p.k_blocks) {
+          // LoRA expand passes: D += A_lora . V_hi^T + A_lora . V_lo^T over the packed K of this pass
+          const uint32_t a0 = ptx::smem_u32(smem + S::kVOff);
+          const uint32_t vh0 = a0 + S::kLoraA, vl0 = vh0 + S::kLoraV;
+          constexpr uint32_t kSbo = (S::kKp / 8) * 128;  // 8-row group stride
+          for (;;) {
+            ptx::mbar_wait(lora_full, lf_phase);
+            lf_phase ^= 1u;
+            ptx::tc_fence_after();
+            const int kp = s_misc[2], last = s_misc[3];
+            for (int kk = 0; kk < kp / 16; ++kk) {
+              const uint64_t ad = ptx::sdesc_k_none(a0 + kk * 256, 128, kSbo);
+              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vh0 + kk * 256, 128, kSbo), idesc, 1u);
+              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vl0 + kk * 256, 128, kSbo), idesc, 1u);
+            }
+            ptx::mma_commit(lora_empty);
+            if (last) break;
           }
         }
         ptx::mma_commit(&tfull[acc]);
@@ -401,6 +434,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     uint32_t acc_phase = 0;
     bool first_seg = true;
     int pre_n = -1;
+    uint32_t le_phase = 0;
     for (int u = u_lo; u < u_hi;) {
       const int tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks;
@@ -428,17 +462,139 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               }
           }
           s_lead[i] = lead;
+          if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups)
+            bool f = a >= 0;
+            for (int i2 = 0; i2 < i && f; ++i2) f = (s_ids[i2] != a);
+            s_mem[i] = f ? 1 : 0;
+          }
         }
         ptx::named_bar_sync(1, 128);
         cur_nt = nt;
       }
-      // LoRA term of the first 16 tokens, gathered BEFORE waiting for the accumulator so it overlaps
-      // this tile's mainloop.
+      if (p.tcx && kb1 == p.k_blocks) {
+        // ---- tensor-core expand operands of this tile, built while its weights stream -------------------
+        // rank columns of the tile's (adapter group, slice) pairs packed in passes of kKp; per pass:
+        // A[n][k] = B_{a,j}[k][n] (rows n of slice j inside its expand window, else 0) and
+        // V[t][k] = v[t][j][k] split into bf16 hi + lo (tokens of group a, else 0); the MMA warp adds
+        // A.V_hi^T + A.V_lo^T into this tile's TMEM accumulator (fp32) -- one rounding at the store.
+        const int n0 = mt * kUmmaBM;
+        int jlo = 0, jhi = 0;
+        for (int q2 = 1; q2 < p.g.J; ++q2) {
+          if (n0 >= p.g.col0[q2]) jlo = q2;
+          if (min(n0 + kUmmaBM - 1, p.g.M - 1) >= p.g.col0[q2]) jhi = q2;
+        }
+        int jn = 0;
+        for (int q2 = 1; q2 < p.g.J; ++q2)
+          if (n >= p.g.col0[q2]) jn = q2;
+        const bool in_win = n < p.g.M && n >= p.g.e_lo[jn] && n < p.g.e_hi[jn];
+        uint8_t* la = smem + S::kVOff;
+        uint8_t* lvh = la + S::kLoraA;
+        uint8_t* lvl = lvh + S::kLoraV;
+        constexpr int KC = S::kKp / 8;  // core-matrix columns per pass
+        int ci = 0, cj = jlo, ccol = 0;
+        bool done = false;
+        while (!done) {
+          int ncol = 0;
+          int cola[KC], colj[KC], colk[KC];
+#pragma unroll
+          for (int c = 0; c < KC; ++c) cola[c] = -1, colj[c] = 0, colk[c] = 0;
+          while (ncol < KC) {  // uniform walk: every thread computes the same pass
+            if (ci >= tv) {
+              done = true;
+              break;
+            }
+            if (!s_mem[ci]) {
+              ++ci;
+              cj = jlo;
+              ccol = 0;
+              continue;
+            }
+            const int a = s_ids[ci];
+            if (ccol >= (p.tab[a].re + 7) / 8) {
+              ccol = 0;
+              if (++cj > jhi) {
+                cj = jlo;
+                ++ci;
+              }
+              continue;
+            }
+#pragma unroll
+            for (int c = 0; c < KC; ++c)
+              if (c == ncol) cola[c] = a, colj[c] = cj, colk[c] = ccol * 8;
+            ++ncol;
+            ++ccol;
+          }
+          if (!done && ci >= tv) done = true;
+          ptx::mbar_wait(lora_empty, le_phase ^ 1u);  // previous pass's MMAs have read the operands
+          // A: this thread's output column n, 8 rank rows per 16-byte chunk
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            uint32_t w4[4] = {0u, 0u, 0u, 0u};
+            if (c < ncol && in_win && colj[c] == jn) {
+              const int a = cola[c], re = p.tab[a].re, ldb = p.g.e_hi[jn] - p.g.e_lo[jn];
+              const uint16_t* Bp = reinterpret_cast<const uint16_t*>(p.arena + p.tab[a].offB[jn]) + (n - p.g.e_lo[jn]);
+#pragma unroll
+              for (int q2 = 0; q2 < 8; q2 += 2) {
+                const int k = colk[c] + q2;
+                const uint32_t lo16 = (k < re) ? (uint32_t)__ldg(Bp + (size_t)k * ldb) : 0u;
+                const uint32_t hi16 = (k + 1 < re) ? (uint32_t)__ldg(Bp + (size_t)(k + 1) * ldb) : 0u;
+                w4[q2 / 2] = lo16 | (hi16 << 16);
+              }
+            }
+            *reinterpret_cast<uint4*>(la + ((row >> 3) * KC + c) * 128 + (row & 7) * 16) =
+                make_uint4(w4[0], w4[1], w4[2], w4[3]);
+          }
+          // V_hi / V_lo: (token, column) pairs over the 128 threads
+          for (int idx = etid; idx < BN * KC; idx += 128) {
+            const int t = idx / KC, c = idx - t * KC;
+            float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            int ca = -1, cjj = 0, ck = 0;
+#pragma unroll
+            for (int c2 = 0; c2 < KC; ++c2)
+              if (c2 == c) ca = cola[c2], cjj = colj[c2], ck = colk[c2];
+            if (c < ncol && t < tv && s_ids[t] == ca) {
+              const int re = p.tab[ca].re, rcc = re / p.g.C;
+#pragma unroll
+              for (int q2 = 0; q2 < 8; ++q2) {
+                const int k = ck + q2;
+                if (k < re) {
+                  const int ch = k / rcc, kk = k - ch * rcc;
+                  f[q2] = __ldg(p.v + ((size_t)(ch * p.T + t0 + t) * p.g.J + cjj) * p.g.Rc + kk);
+                }
+              }
+            }
+            uint32_t h4[4], l4[4];
+#pragma unroll
+            for (int q2 = 0; q2 < 8; q2 += 2) {
+              const __nv_bfloat16 h0 = __float2bfloat16_rn(f[q2]), h1 = __float2bfloat16_rn(f[q2 + 1]);
+              const __nv_bfloat16 l0 = __float2bfloat16_rn(f[q2] - __bfloat162float(h0));
+              const __nv_bfloat16 l1 = __float2bfloat16_rn(f[q2 + 1] - __bfloat162float(h1));
+              h4[q2 / 2] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+              l4[q2 / 2] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+            }
+            const int off = ((t >> 3) * KC + c) * 128 + (t & 7) * 16;
+            *reinterpret_cast<uint4*>(lvh + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+            *reinterpret_cast<uint4*>(lvl + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
+          }
+          ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
+          if (etid == 0) {
+            s_misc[2] = ((ncol * 8 + 15) / 16) * 16;
+            s_misc[3] = done ? 1 : 0;
+          }
+          ptx::mbar_arrive(lora_full);
+          le_phase ^= 1u;
+        }
+      }
+      // LoRA term of the first 16 tokens on CUDA cores (when not on the tensor cores), gathered BEFORE
+      // waiting for the accumulator so it overlaps this tile's mainloop.
       float lr[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) lr[i] = 0.f;
       if (!first_seg && n != pre_n) pre.a = -1;  // cached B rows belong to another output column
       pre_n = n;
-      lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, &pre, s_v, S::kVFloats,
-                   etid);
+      if (!p.tcx)
+        lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, &pre, s_v, S::kVFloats,
+                     etid);
       if (first_seg && etid == 0) UMMA_TRACE(15);
       first_seg = false;
       ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -453,7 +609,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::tmem_ld_32x32b_x16(taddr + c0, r);
         ptx::tmem_ld_wait();
         if (whole) {
-          if (c0 > 0)
+          if (c0 > 0 && !p.tcx)
             lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T,
                          &pre, s_v, S::kVFloats, etid);
           if (n < p.M) {
@@ -493,7 +649,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           const int c_first = umma_cta_of(ts, UNITS, GRID);
           const int c_last = umma_cta_of(ts + p.k_blocks - 1, UNITS, GRID);
           for (int c0 = 0; c0 < tv; c0 += 16) {
-            if (c0 > 0 || tv > 16)
+            if ((c0 > 0 || tv > 16) && !p.tcx)
               lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v,
                            p.T, &pre, s_v, S::kVFloats, etid);
             const int nq = min(4, (tv - c0 + 3) / 4);  // float4 groups holding valid tokens
@@ -674,6 +830,16 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
 // ------------------------------------------------------------------------------------------------
 inline long long* g_umma_trace = nullptr;  // profiling hook (bdlora_debug_trace)
 
+// LoRA expand on the tensor cores (default) -- BDLORA_TC_EXPAND=0 selects the CUDA-core epilogue expand.
+inline bool tensor_expand_enabled() {
+  static int env = -1;
+  if (env < 0) {
+    const char* s = getenv("BDLORA_TC_EXPAND");
+    env = (s && s[0] == '0') ? 0 : 1;
+  }
+  return env == 1;
+}
+
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
 
 // Workspace: [sync: 3 ints, 256 B][tile counters][split-tile partials]
@@ -772,7 +938,8 @@ inline int umma_dispatch_bn(int BN, const UmmaParams& p, const CUtensorMap& tmW,
 // Returns 0 on launch, non-zero if the shape is not handled here.
 inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_bfloat16* W, const int* ids,
                        const SlotEntry* tab, const __nv_bfloat16* arena, const float* v, __nv_bfloat16* Y, void* ws,
-                       int num_sms, cudaStream_t st, int pdl = 0, float* v_fused = nullptr, int rs_max = 0) {
+                       int num_sms, cudaStream_t st, int pdl = 0, float* v_fused = nullptr, int rs_max = 0,
+                       int tcx = 0) {
   if (!umma_eligible(g, T)) return 1;
   if (v_fused && T > kFuseMaxT) return 1;
   const int BN = umma_bn_for(T);
@@ -815,6 +982,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.fuse = v_fused ? 1 : 0;
   p.v_out = v_fused;
   p.rs_max = rs_max;
+  p.tcx = (v_fused || !tensor_expand_enabled()) ? 0 : tcx;
   if (v_fused) p.v = v_fused;
   p.pdl = pdl;
   p.trace = g_umma_trace;
@@ -860,6 +1028,7 @@ inline int umma_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, cons
   p.part = (float*)((char*)ws + 256 + cnt_bytes);
   p.X = X;
   p.fuse = 0;
+  p.tcx = 0;
   p.v_out = v_out;
   p.route = route;
   p.pdl = pdl;

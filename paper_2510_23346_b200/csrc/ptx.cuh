@@ -122,6 +122,18 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// Shared-memory matrix descriptor, K-major, SWIZZLE_NONE ("interleaved") canonical layout: core
+// matrices of 8 rows x 16 B stored as 128 contiguous bytes; LBO = byte stride between K-adjacent core
+// matrices, SBO = byte stride between 8-row groups; version 1 (sm_100), layout type 0.
+__device__ __forceinline__ uint64_t sdesc_k_none(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
 // Instruction descriptor kind::f16: D fp32 [4,6)=1, A bf16 [7,10)=1, B bf16 [10,13)=1, both K-major,
 // N>>3 at [17,23), M>>4 at [24,29).
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {

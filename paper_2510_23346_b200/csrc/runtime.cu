@@ -300,7 +300,7 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, T, (const __nv_bfloat16*)W, ids, p->d_tab,
                               (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
-                              p->num_sms, st, pdl);
+                              p->num_sms, st, pdl, nullptr, 0, /*tcx=*/1);
     if (rc == 0) {
       count_launch();
       CU_TRY(cudaGetLastError());
