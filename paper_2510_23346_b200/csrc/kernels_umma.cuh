@@ -416,10 +416,15 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             }
         }
         s_lead[i] = lead;
+        if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups)
+          bool f = a >= 0;
+          for (int i2 = 0; i2 < i && f; ++i2) f = (s_ids[i2] != a);
+          s_mem[i] = f ? 1 : 0;
+        }
       }
       ptx::named_bar_sync(1, 128);
       cur_nt = nt;
-      lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
+      if (!p.tcx) lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
     }
     if (p.fuse) {
       // every unit of the launch published before any expand reads v
