@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     n_items = p.route[RouteLayout::kHdr + 1];
     M_TILES = (n_items + 7) / 8;
     UNITS = M_TILES * p.n_tiles * p.k_blocks;
-    GRID = max(1, min((int)gridDim.x, UNITS / 8));
+    // >= 32 k-blocks per CTA: the shrink is small, a split tile's fix-up (one partial per contributor and
+    // token chunk) costs more than the streaming it parallelises
+    GRID = max(1, min((int)gridDim.x, UNITS / 32));
   }
   const bool active = cta < GRID && UNITS > 0;
   const int u_lo = active ? umma_u_lo(cta, UNITS, GRID) : 0;
