@@ -58,9 +58,12 @@ __device__ __forceinline__ int block_excl_scan_1024(int x, int* s_warp, int* tot
 }
 
 __global__ void __launch_bounds__(1024) route_kernel(const int* __restrict__ ids, int T,
-                                                     const SlotEntry* __restrict__ tab, Geom g, int* __restrict__ route) {
+                                                     const SlotEntry* __restrict__ tab, Geom g, int* __restrict__ route,
+                                                     float* __restrict__ v, int nv) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");  // ids may come from the preceding kernel
+  // the shrink GEMM accumulates v with fp32 reductions: start from zero
+  for (int i = threadIdx.x; i < nv; i += 1024) v[i] = 0.f;
   __shared__ int s_seg_id[kRouteMaxSeg];
   __shared__ int s_warp[33];
   __shared__ int s_nseg, s_ngrp;

@@ -129,9 +129,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     n_items = p.route[RouteLayout::kHdr + 1];
     M_TILES = (n_items + 7) / 8;
     UNITS = M_TILES * p.n_tiles * p.k_blocks;
-    // >= 32 k-blocks per CTA: the shrink is small, a split tile's fix-up (one partial per contributor and
-    // token chunk) costs more than the streaming it parallelises
-    GRID = max(1, min((int)gridDim.x, UNITS / 32));
+    // split-K contributors add their share of v with fp32 reductions (no fix-up round trip); >= 8
+    // k-blocks per CTA
+    GRID = max(1, min((int)gridDim.x, UNITS / 8));
   }
   const bool active = cta < GRID && UNITS > 0;
   const int u_lo = active ? umma_u_lo(cta, UNITS, GRID) : 0;
@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (ptx::elect_one()) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(kUmmaBM, BN);
+      constexpr uint32_t idesc_lora = idesc | (1u << 15);  // A operand MN-major
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -272,10 +273,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             lf_phase ^= 1u;
             ptx::tc_fence_after();
             const int kp = s_misc[2], last = s_misc[3];
-            for (int kk = 0; kk < kp / 16; ++kk) {
-              const uint64_t ad = ptx::sdesc_k_none(a0 + kk * 256, 128, kSbo);
-              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vh0 + kk * 256, 128, kSbo), idesc, 1u);
-              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vl0 + kk * 256, 128, kSbo), idesc, 1u);
+            for (int kk = 0; kk < kp / 16; ++kk) {  // A is MN-major (idesc_ab), V K-major
+              const uint64_t ad = ptx::sdesc_k_none(a0 + kk * 4096, /*LBO: k-group*/ 2048, /*SBO: n-group*/ 128);
+              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vh0 + kk * 256, 128, kSbo), idesc_lora, 1u);
+              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vl0 + kk * 256, 128, kSbo), idesc_lora, 1u);
             }
             ptx::mma_commit(lora_empty);
             if (last) break;
@@ -533,23 +534,35 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           }
           if (!done && ci >= tv) done = true;
           ptx::mbar_wait(lora_empty, le_phase ^ 1u);  // previous pass's MMAs have read the operands
-          // A: this thread's output column n, 8 rank rows per 16-byte chunk
+          // A = B-slab^T in the MN-major no-swizzle layout: a 16-byte chunk is 8 consecutive output columns
+          // of one rank row k -- exactly 16 contiguous bytes of B's row k, so the gather is a plain
+          // coalesced LDG.128 -> STS.128 (core matrix (n-group, k-group) at (kg * 16 + ng) * 128, row k % 8)
+          for (int idx = etid; idx < S::kKp * 16; idx += 128) {
+            const int kr = idx >> 4, ng = idx & 15, c = kr >> 3;
+            int ca = -1, cjj = 0, ck = 0;
 #pragma unroll
-          for (int c = 0; c < KC; ++c) {
-            uint32_t w4[4] = {0u, 0u, 0u, 0u};
-            if (c < ncol && in_win && colj[c] == jn) {
-              const int a = cola[c], re = p.tab[a].re, ldb = p.g.e_hi[jn] - p.g.e_lo[jn];
-              const uint16_t* Bp = reinterpret_cast<const uint16_t*>(p.arena + p.tab[a].offB[jn]) + (n - p.g.e_lo[jn]);
+            for (int c2 = 0; c2 < KC; ++c2)
+              if (c2 == c) ca = cola[c2], cjj = colj[c2], ck = colk[c2];
+            uint4 val = make_uint4(0u, 0u, 0u, 0u);
+            const int k = ck + (kr & 7);
+            if (c < ncol && ca >= 0 && k < p.tab[ca].re) {
+              const int lo = p.g.e_lo[cjj], hi = min(p.g.e_hi[cjj], p.g.M), ldb = p.g.e_hi[cjj] - lo;
+              const int nlo = n0 + ng * 8;
+              const uint16_t* Brow = reinterpret_cast<const uint16_t*>(p.arena + p.tab[ca].offB[cjj]) + (size_t)k * ldb;
+              if (nlo >= lo && nlo + 8 <= hi && (((uintptr_t)(Brow + (nlo - lo))) & 15) == 0) {
+                val = __ldg(reinterpret_cast<const uint4*>(Brow + (nlo - lo)));
+              } else {
+                uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-              for (int q2 = 0; q2 < 8; q2 += 2) {
-                const int k = colk[c] + q2;
-                const uint32_t lo16 = (k < re) ? (uint32_t)__ldg(Bp + (size_t)k * ldb) : 0u;
-                const uint32_t hi16 = (k + 1 < re) ? (uint32_t)__ldg(Bp + (size_t)(k + 1) * ldb) : 0u;
-                w4[q2 / 2] = lo16 | (hi16 << 16);
+                for (int e2 = 0; e2 < 8; ++e2) {
+                  const int nn = nlo + e2;
+                  const uint32_t h = (nn >= lo && nn < hi) ? (uint32_t)__ldg(Brow + (nn - lo)) : 0u;
+                  w[e2 >> 1] |= h << ((e2 & 1) * 16);
+                }
+                val = make_uint4(w[0], w[1], w[2], w[3]);
               }
             }
-            *reinterpret_cast<uint4*>(la + ((row >> 3) * KC + c) * 128 + (row & 7) * 16) =
-                make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            *reinterpret_cast<uint4*>(la + ((kr >> 3) * 16 + ng) * 128 + (kr & 7) * 16) = val;
           }
           // V_hi / V_lo: (token, column) pairs over the 128 threads
           for (int idx = etid; idx < BN * KC; idx += 128) {
@@ -561,12 +574,19 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               if (c2 == c) ca = cola[c2], cjj = colj[c2], ck = colk[c2];
             if (c < ncol && t < tv && s_ids[t] == ca) {
               const int re = p.tab[ca].re, rcc = re / p.g.C;
+              const float* vrow = p.v + ((size_t)(t0 + t) * p.g.J + cjj) * p.g.Rc + ck;
+              if (p.g.C == 1 && ck + 8 <= re && (p.g.Rc & 3) == 0) {
+                const float4 f0 = __ldg(reinterpret_cast<const float4*>(vrow));
+                const float4 f1 = __ldg(reinterpret_cast<const float4*>(vrow + 4));
+                f[0] = f0.x, f[1] = f0.y, f[2] = f0.z, f[3] = f0.w, f[4] = f1.x, f[5] = f1.y, f[6] = f1.z, f[7] = f1.w;
+              } else {
 #pragma unroll
-              for (int q2 = 0; q2 < 8; ++q2) {
-                const int k = ck + q2;
-                if (k < re) {
-                  const int ch = k / rcc, kk = k - ch * rcc;
-                  f[q2] = __ldg(p.v + ((size_t)(ch * p.T + t0 + t) * p.g.J + cjj) * p.g.Rc + kk);
+                for (int q2 = 0; q2 < 8; ++q2) {
+                  const int k = ck + q2;
+                  if (k < re) {
+                    const int ch = k / rcc, kk = k - ch * rcc;
+                    f[q2] = __ldg(p.v + ((size_t)(ch * p.T + t0 + t) * p.g.J + cjj) * p.g.Rc + kk);
+                  }
                 }
               }
             }
@@ -744,73 +764,20 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           uint32_t r[16];
           ptx::tmem_ld_32x32b_x16(taddr + c0, r);
           ptx::tmem_ld_wait();
-          if (whole) {
-            if (va >= 0) {
+          if (va >= 0) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (c0 + i < tv && s_ids[c0 + i] == va)
-                  p.v_out[((size_t)(t0 + c0 + i) * p.g.J + vj) * p.g.Rc + vk] = vsc * __uint_as_float(r[i]);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              __stcg(reinterpret_cast<float4*>(my_part + c0 + i),
-                     make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
-                                 __uint_as_float(r[i + 3])));
+            for (int i = 0; i < 16; ++i)
+              if (c0 + i < tv && s_ids[c0 + i] == va) {
+                float* dst = p.v_out + ((size_t)(t0 + c0 + i) * p.g.J + vj) * p.g.Rc + vk;
+                if (whole)
+                  *dst = vsc * __uint_as_float(r[i]);
+                else
+                  atomicAdd(dst, vsc * __uint_as_float(r[i]));  // split-K share (v zeroed by route_kernel)
+              }
           }
         }
         ptx::tc_fence_before();
         ptx::mbar_arrive(&tempty[acc]);
-        if (!whole) {
-          ptx::named_bar_sync(1, 128);
-          if (etid == 0) {
-            const int got = kb1 - kb0;
-            const int old = ptx::atom_add_acq_rel_gpu(p.tile_cnt + tile, got);
-            *s_last = (old + got == p.k_blocks);
-          }
-          ptx::named_bar_sync(1, 128);
-          if (*s_last) {
-            const int ts = tile * p.k_blocks;
-            const int c_first = umma_cta_of(ts, UNITS, GRID);
-            const int c_last = umma_cta_of(ts + p.k_blocks - 1, UNITS, GRID);
-            for (int c0 = 0; c0 < tv; c0 += 16) {
-              const int nq = min(4, (tv - c0 + 3) / 4);
-              float y[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) y[i] = 0.f;
-              for (int cb = c_first; cb <= c_last; cb += 8) {
-                float4 buf[8][4];
-#pragma unroll
-                for (int cc = 0; cc < 8; ++cc) {
-                  const int c = cb + cc;
-                  const int sl = (c <= c_last && ts > umma_u_lo(c, UNITS, GRID)) ? 1 : 0;
-                  const float4* src = reinterpret_cast<const float4*>(
-                      p.part + ((size_t)(min(c, c_last) * 2 + sl) * kUmmaBM + row) * BN + c0);
-#pragma unroll
-                  for (int g4 = 0; g4 < 4; ++g4)
-                    buf[cc][g4] = (c <= c_last && g4 < nq) ? __ldcg(src + g4) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-#pragma unroll
-                for (int cc = 0; cc < 8; ++cc)
-#pragma unroll
-                  for (int g4 = 0; g4 < 4; ++g4) {
-                    y[4 * g4] += buf[cc][g4].x;
-                    y[4 * g4 + 1] += buf[cc][g4].y;
-                    y[4 * g4 + 2] += buf[cc][g4].z;
-                    y[4 * g4 + 3] += buf[cc][g4].w;
-                  }
-              }
-              if (va >= 0) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                  if (c0 + i < tv && s_ids[c0 + i] == va)
-                    p.v_out[((size_t)(t0 + c0 + i) * p.g.J + vj) * p.g.Rc + vk] = vsc * y[i];
-              }
-            }
-            if (etid == 0) p.tile_cnt[tile] = 0;
-          }
-          ptx::named_bar_sync(1, 128);
-        }
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
         u += kb1 - kb0;

@@ -225,7 +225,8 @@ int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CU_TRY(cudaLaunchKernelEx(&cfg, bdl::route_kernel, ids, T, (const SlotEntry*)p->d_tab, p->g, route));
+    CU_TRY(cudaLaunchKernelEx(&cfg, bdl::route_kernel, ids, T, (const SlotEntry*)p->d_tab, p->g, route, v,
+                              (int)(T * p->g.J * p->g.Rc)));
     count_launch();
     int rc = bdl::umma_shrink_launch(p->g, (const __nv_bfloat16*)X, T, ids, p->d_tab, route, p->amap, v, items,
                                      (char*)ws + L.off_shrink, p->num_sms, st, g_pdl);
