@@ -80,7 +80,7 @@ struct UmmaSmem {
   static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kVOff = kBarOff + 256 + 5120 + 256;          // after barriers/flags, ids/leaders/shrink
+  static constexpr int kVOff = kBarOff + 256 + 5120 + 512;          // after barriers/flags, ids/leaders/shrink
   static constexpr int kVFloats = 4096;                              // 16 KB v staging (CUDA-core expand)
   // tensor-core expand operands (share the region with the v staging): A = B-slab^T [128 x Kp],
   // V_hi / V_lo = bf16 split of v [BN x Kp], K-major, no-swizzle core-matrix layout
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_isl = s_mem + 256;                      // [T] 1 if the token is the first of its adapter id
   float* s_red = (float*)(s_isl + 256);          // [4][4] cross-warp partial dots
   int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count, [2] pass K, [3] last
-  int* s_pcol = s_misc + 16;                     // [8][3] tensor-core expand pass columns (a, j, k base)
+  int* s_pcol = s_misc + 16;                     // [8][6] tensor-core expand pass columns (a, j, k0, re, boff lo/hi)
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -499,56 +499,60 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         uint8_t* lvh = la + S::kLoraA;
         uint8_t* lvl = lvh + S::kLoraV;
         constexpr int KC = S::kKp / 8;  // core-matrix columns per pass
-        int ci = 0, cj = jlo, ccol = 0;
+        int ci = 0, cj = jlo, ccol = 0;  // pass cursor (thread 0)
         bool done = false;
         while (!done) {
-          int ncol = 0;
-          int cola[KC], colj[KC], colk[KC];
-#pragma unroll
-          for (int c = 0; c < KC; ++c) cola[c] = -1, colj[c] = 0, colk[c] = 0;
-          while (ncol < KC) {  // uniform walk: every thread computes the same pass
-            if (ci >= tv) {
-              done = true;
-              break;
-            }
-            if (!s_mem[ci]) {
-              ++ci;
-              cj = jlo;
-              ccol = 0;
-              continue;
-            }
-            const int a = s_ids[ci];
-            if (ccol >= (p.tab[a].re + 7) / 8) {
-              ccol = 0;
-              if (++cj > jhi) {
-                cj = jlo;
+          if (etid == 0) {  // next pass: up to KC columns of 8 rank rows, metadata for all threads
+            int ncol = 0;
+            while (ncol < KC) {
+              if (ci >= tv) break;
+              if (!s_mem[ci]) {
                 ++ci;
+                cj = jlo;
+                ccol = 0;
+                continue;
               }
-              continue;
+              const int a = s_ids[ci];
+              const int re = p.tab[a].re;
+              if (ccol >= (re + 7) / 8) {
+                ccol = 0;
+                if (++cj > jhi) {
+                  cj = jlo;
+                  ++ci;
+                }
+                continue;
+              }
+              const long long boff = p.tab[a].offB[cj];
+              int* pc = s_pcol + ncol * 6;
+              pc[0] = a, pc[1] = cj, pc[2] = ccol * 8, pc[3] = re, pc[4] = (int)(boff & 0xffffffff), pc[5] = (int)(boff >> 32);
+              ++ncol;
+              ++ccol;
             }
-#pragma unroll
-            for (int c = 0; c < KC; ++c)
-              if (c == ncol) cola[c] = a, colj[c] = cj, colk[c] = ccol * 8;
-            ++ncol;
-            ++ccol;
+            // look ahead: is anything left after this pass?
+            while (ci < tv && !s_mem[ci]) ++ci;
+            s_misc[4] = ncol;
+            s_misc[5] = (ci >= tv) ? 1 : 0;
           }
-          if (!done && ci >= tv) done = true;
+          ptx::named_bar_sync(1, 128);
+          const int ncol = s_misc[4];
+          done = s_misc[5] != 0;
           ptx::mbar_wait(lora_empty, le_phase ^ 1u);  // previous pass's MMAs have read the operands
           // A = B-slab^T in the MN-major no-swizzle layout: a 16-byte chunk is 8 consecutive output columns
           // of one rank row k -- exactly 16 contiguous bytes of B's row k, so the gather is a plain
           // coalesced LDG.128 -> STS.128 (core matrix (n-group, k-group) at (kg * 16 + ng) * 128, row k % 8)
-          for (int idx = etid; idx < S::kKp * 16; idx += 128) {
-            const int kr = idx >> 4, ng = idx & 15, c = kr >> 3;
-            int ca = -1, cjj = 0, ck = 0;
 #pragma unroll
-            for (int c2 = 0; c2 < KC; ++c2)
-              if (c2 == c) ca = cola[c2], cjj = colj[c2], ck = colk[c2];
+          for (int it = 0; it < S::kKp * 16 / 128; ++it) {
+            const int idx = etid + it * 128;
+            const int kr = idx >> 4, ng = idx & 15, c = kr >> 3;
+            const int* pc = s_pcol + c * 6;
             uint4 val = make_uint4(0u, 0u, 0u, 0u);
-            const int k = ck + (kr & 7);
-            if (c < ncol && ca >= 0 && k < p.tab[ca].re) {
+            const int k = pc[2] + (kr & 7);
+            if (c < ncol && k < pc[3]) {
+              const int cjj = pc[1];
               const int lo = p.g.e_lo[cjj], hi = min(p.g.e_hi[cjj], p.g.M), ldb = p.g.e_hi[cjj] - lo;
               const int nlo = n0 + ng * 8;
-              const uint16_t* Brow = reinterpret_cast<const uint16_t*>(p.arena + p.tab[ca].offB[cjj]) + (size_t)k * ldb;
+              const long long boff = (long long)(unsigned)pc[4] | ((long long)pc[5] << 32);
+              const uint16_t* Brow = reinterpret_cast<const uint16_t*>(p.arena + boff) + (size_t)k * ldb;
               if (nlo >= lo && nlo + 8 <= hi && (((uintptr_t)(Brow + (nlo - lo))) & 15) == 0) {
                 val = __ldg(reinterpret_cast<const uint4*>(Brow + (nlo - lo)));
               } else {
@@ -565,15 +569,15 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             *reinterpret_cast<uint4*>(la + ((kr >> 3) * 16 + ng) * 128 + (kr & 7) * 16) = val;
           }
           // V_hi / V_lo: (token, column) pairs over the 128 threads
-          for (int idx = etid; idx < BN * KC; idx += 128) {
-            const int t = idx / KC, c = idx - t * KC;
-            float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            int ca = -1, cjj = 0, ck = 0;
 #pragma unroll
-            for (int c2 = 0; c2 < KC; ++c2)
-              if (c2 == c) ca = cola[c2], cjj = colj[c2], ck = colk[c2];
-            if (c < ncol && t < tv && s_ids[t] == ca) {
-              const int re = p.tab[ca].re, rcc = re / p.g.C;
+          for (int it = 0; it < (BN * KC + 127) / 128; ++it) {
+            const int idx = etid + it * 128;
+            if (idx >= BN * KC) break;
+            const int t = idx / KC, c = idx - t * KC;
+            const int* pc = s_pcol + c * 6;
+            float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (c < ncol && t < tv && s_ids[t] == pc[0]) {
+              const int cjj = pc[1], ck = pc[2], re = pc[3], rcc = re / p.g.C;
               const float* vrow = p.v + ((size_t)(t0 + t) * p.g.J + cjj) * p.g.Rc + ck;
               if (p.g.C == 1 && ck + 8 <= re && (p.g.Rc & 3) == 0) {
                 const float4 f0 = __ldg(reinterpret_cast<const float4*>(vrow));
@@ -609,6 +613,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             s_misc[3] = done ? 1 : 0;
           }
           ptx::mbar_arrive(lora_full);
+          ptx::named_bar_sync(1, 128);  // s_pcol / s_misc reused by the next pass
           le_phase ^= 1u;
         }
       }
