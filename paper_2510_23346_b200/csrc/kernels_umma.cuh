@@ -248,6 +248,26 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        // LoRA expand passes (tensor-core expand duty = this CTA finishes the tile's k range): issued as soon
+        // as the epilogue warps have built them, interleaved with the base k-blocks (accumulation order is
+        // free in fp32), so the operand gathers overlap the weight stream instead of trailing it
+        const bool lduty = (MODE == 0) && p.tcx && kb1 == p.k_blocks;
+        bool ldone = !lduty;
+        const uint32_t la0 = ptx::smem_u32(smem + S::kVOff);
+        auto lora_pass = [&]() {
+          constexpr uint32_t kSbo = (S::kKp / 8) * 128;  // V: 8-row group stride
+          const uint32_t vh0 = la0 + S::kLoraA, vl0 = vh0 + S::kLoraV;
+          lf_phase ^= 1u;
+          ptx::tc_fence_after();
+          const int kp = s_misc[2], last = s_misc[3];
+          for (int kk = 0; kk < kp / 16; ++kk) {  // A is MN-major (idesc_lora), V K-major
+            const uint64_t ad = ptx::sdesc_k_none(la0 + kk * 4096, /*LBO: k-group*/ 2048, /*SBO: n-group*/ 128);
+            ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vh0 + kk * 256, 128, kSbo), idesc_lora, 1u);
+            ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vl0 + kk * 256, 128, kSbo), idesc_lora, 1u);
+          }
+          ptx::mma_commit(lora_empty);
+          if (last) ldone = true;
+        };
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
@@ -262,8 +282,13 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             stage = 0;
             phase ^= 1;
           }
+          if (!ldone && ptx::mbar_test(lora_full, lf_phase)) lora_pass();  // D already initialised (kb0 done)
         }
-        if (MODE == 0 && p.tcx && kb1 == p.k_blocks) {
+        while (!ldone) {
+          ptx::mbar_wait(lora_full, lf_phase);
+          lora_pass();
+        }
+        if (false) {
           // LoRA expand passes: D += A_lora . V_hi^T + A_lora . V_lo^T over the packed K of this pass
           const uint32_t a0 = ptx::smem_u32(smem + S::kVOff);
           const uint32_t vh0 = a0 + S::kLoraA, vl0 = vh0 + S::kLoraV;
