@@ -77,7 +77,7 @@ struct UmmaSmem {
   static constexpr int kWBytes = kUmmaBM * kUmmaBK * 2;  // 16 KB
   static constexpr int kXBytes = BN * kUmmaBK * 2;
   static constexpr int kStageBytes = kWBytes + kXBytes;
-  static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 7 : BN <= 128 ? 6 : 4);
+  static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 7 : BN <= 128 ? 5 : 4);
   static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
   static constexpr int kVOff = kBarOff + 256 + 5120 + 512;          // after barriers/flags, ids/leaders/shrink
@@ -89,7 +89,8 @@ struct UmmaSmem {
   static constexpr int kLoraV = BN * kKp * 2;
   static constexpr int kLoraBytes = kLoraA + 2 * kLoraV;
   static constexpr int kRegion = kLoraBytes > kVFloats * 4 ? kLoraBytes : kVFloats * 4;
-  static constexpr int kBytes = kVOff + kRegion + 1024;              // + alignment slack
+  static constexpr int kMetaOff = kVOff + kRegion;                  // [BN][8] ints: leader re / offB (tc expand)
+  static constexpr int kBytes = kMetaOff + BN * 8 * 4 + 1024;        // + alignment slack
 };
 
 template <int BN, int MODE>
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   float* s_red = (float*)(s_isl + 256);          // [4][4] cross-warp partial dots
   int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count, [2] pass K, [3] last
   int* s_pcol = s_misc + 16;                     // [8][6] tensor-core expand pass columns (a, j, k0, re, boff lo/hi)
+  int* s_gmeta = (int*)(smem + S::kMetaOff);     // [BN][8] per leader token: re, offB[0..2] (lo, hi)
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -444,10 +446,20 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             }
         }
         s_lead[i] = lead;
-        if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups)
+        if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups) + its slot metadata
           bool f = a >= 0;
           for (int i2 = 0; i2 < i && f; ++i2) f = (s_ids[i2] != a);
           s_mem[i] = f ? 1 : 0;
+          if (f) {
+            int* gm = s_gmeta + i * 8;
+            gm[0] = p.tab[a].re;
+#pragma unroll
+            for (int jj = 0; jj < kMaxSlices; ++jj) {
+              const long long ob = p.tab[a].offB[jj];
+              gm[1 + 2 * jj] = (int)(ob & 0xffffffff);
+              gm[2 + 2 * jj] = (int)(ob >> 32);
+            }
+          }
         }
       }
       ptx::named_bar_sync(1, 128);
@@ -495,10 +507,20 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               }
           }
           s_lead[i] = lead;
-          if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups)
+          if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups) + its slot metadata
             bool f = a >= 0;
             for (int i2 = 0; i2 < i && f; ++i2) f = (s_ids[i2] != a);
             s_mem[i] = f ? 1 : 0;
+            if (f) {
+              int* gm = s_gmeta + i * 8;
+              gm[0] = p.tab[a].re;
+#pragma unroll
+              for (int jj = 0; jj < kMaxSlices; ++jj) {
+                const long long ob = p.tab[a].offB[jj];
+                gm[1 + 2 * jj] = (int)(ob & 0xffffffff);
+                gm[2 + 2 * jj] = (int)(ob >> 32);
+              }
+            }
           }
         }
         ptx::named_bar_sync(1, 128);
@@ -538,7 +560,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 continue;
               }
               const int a = s_ids[ci];
-              const int re = p.tab[a].re;
+              const int* gm = s_gmeta + ci * 8;
+              const int re = gm[0];
               if (ccol >= (re + 7) / 8) {
                 ccol = 0;
                 if (++cj > jhi) {
@@ -547,9 +570,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                 }
                 continue;
               }
-              const long long boff = p.tab[a].offB[cj];
               int* pc = s_pcol + ncol * 6;
-              pc[0] = a, pc[1] = cj, pc[2] = ccol * 8, pc[3] = re, pc[4] = (int)(boff & 0xffffffff), pc[5] = (int)(boff >> 32);
+              pc[0] = a, pc[1] = cj, pc[2] = ccol * 8, pc[3] = re, pc[4] = gm[1 + 2 * cj], pc[5] = gm[2 + 2 * cj];
               ++ncol;
               ++ccol;
             }
