@@ -101,8 +101,16 @@ int bdlora_kernel_launches(int64_t* n);
    the pool's adapter factors must not be written by the kernel immediately preceding a forward on
    the same stream (they are streamed before the dependency resolves).  0 = plain stream order.   */
 int bdlora_set_pdl(int enable);
+/* Decode (T <= 16) LoRA schedule inside the fused single-kernel forward.  The layer is linear in a
+   partition of K (y = sum_seg X_seg W_seg + s (X_seg A_seg) B, regrouping matmul_3/4 and matmul_5/6 of
+   Alg. 1/2), so each CTA streaming a K-range of W can add its own share of the LoRA term:
+   0 = GLOBAL: v = s X A computed once by the grid, every CTA waits for the whole v before its expand;
+   1 = AUTO (default): K-local when the token tile's distinct adapters have sum(r/N) <= 64, else global;
+   2 = K-LOCAL whenever eligible (T <= 16, one v chunk).  Results agree to fp32 summation order.
+   Also settable with the environment variable BDLORA_LOCAL.  E_ARG for other values.                */
+int bdlora_set_decode_lora(int mode);
 /* Profiling hook: if non-NULL, subsequent tensor-core GEMM launches record per-CTA %globaltimer
-   stamps (16 int64 per CTA) into this device buffer (>= 148*16*8 bytes); NULL turns it off.      */
+   stamps (32 int64 per CTA) into this device buffer (>= 148*32*8 bytes); NULL turns it off.      */
 int bdlora_debug_trace(void* device_buffer);
 
 /* ---------------------------------------------------------------- communicator (NCCL) ------- */

@@ -27,7 +27,7 @@ __all__ = [
     "bdlora_load_adapter", "bdlora_unload_adapter", "bdlora_pool_bytes", "bdlora_pool_geometry",
     "bdlora_workspace_bytes", "bdlora_build_segments", "bdlora_column_forward", "bdlora_row_partial",
     "bdlora_row_forward", "slora_column_forward", "slora_row_forward", "bdlora_lora_shrink",
-    "bdlora_base_expand", "bdlora_v_elems", "make_workspace",
+    "bdlora_base_expand", "bdlora_v_elems", "make_workspace", "bdlora_set_decode_lora",
 ]
 
 
@@ -338,6 +338,11 @@ def bdlora_base_expand(pool: Pool, X, W, ids, v, Y, ws, stream=None) -> None:
 def bdlora_debug_trace(buf) -> None:
     """Profiling hook: per-CTA timestamps of subsequent GEMM launches into `buf` (device int64), or None."""
     call("bdlora_debug_trace", None if buf is None else buf.data_ptr())
+
+
+def bdlora_set_decode_lora(mode: int) -> None:
+    """Decode LoRA schedule of the fused forward: 0 global shrink, 1 auto (default), 2 K-local (bdlora.h)."""
+    call("bdlora_set_decode_lora", int(mode))
 
 
 def bdlora_set_pdl(enable: bool) -> None:

@@ -35,6 +35,7 @@ SIGNATURES = {
     "bdlora_kernel_launches": (c_int, [ctypes.POINTER(c_i64)]),
     "bdlora_debug_trace": (c_int, [c_vp]),
     "bdlora_set_pdl": (c_int, [c_int]),
+    "bdlora_set_decode_lora": (c_int, [c_int]),
     "bdlora_comm_unique_id": (c_int, [c_u8p]),
     "bdlora_comm_init": (c_int, [c_u8p, c_int, c_int, c_int, ctypes.POINTER(c_vp)]),
     "bdlora_comm_destroy": (c_int, [c_vp]),

@@ -54,7 +54,17 @@ struct UmmaParams {
   const int* route;  // shrink mode: groups + 16-row A boxes from route_kernel (RouteLayout)
   int* sync;         // fused mode: [0] unit claim counter, [1] units done, [2] CTAs exited (zero between launches)
   long long* trace;  // optional per-CTA timestamps (ns, %globaltimer) for profiling; nullptr = off
+  int local;         // fused mode: 0 = global shrink, 1 = K-local LoRA when the tile's adapters are few, 2 = always
 };
+
+// K-local LoRA (decode, one adapter group per token tile).  The layer is linear in a partition of K:
+//   y_t = sum_seg [ X_t,seg W_seg + s_a (X_t,seg A_a,seg^T) B_a ]
+// so a CTA owning the K-range of a tile segment adds its own share of the LoRA term to its (partial)
+// accumulator.  The shrink rides the weight pipeline: every stage also carries a 16-row TMA box of the
+// adapter's A rows, and the MMA warp accumulates v_seg = A_seg X_seg^T into a second TMEM accumulator
+// (rows >= r/N of that MMA read unrelated shared memory and are ignored: MMA rows are independent).
+// After the last k-block: v_seg (TMEM lanes 0..15) -> smem -> v_seg B on the CUDA cores (16 FMAs/token).
+// No CTA waits for another's shrink (P:400-403 -- matmul_3/4 and matmul_5/6 regrouped over K).
 
 __device__ __forceinline__ long long gtimer() {
   long long t;
@@ -63,7 +73,7 @@ __device__ __forceinline__ long long gtimer() {
 }
 #define UMMA_TRACE(slot)                                              \
   do {                                                                \
-    if (p.trace) p.trace[(size_t)blockIdx.x * 16 + (slot)] = gtimer(); \
+    if (p.trace) p.trace[(size_t)blockIdx.x * 32 + (slot)] = gtimer(); \
   } while (0)
 
 __device__ __forceinline__ int umma_u_lo(long long c, int units, int grid) { return (int)(c * units / grid); }
@@ -76,9 +86,12 @@ template <int BN>
 struct UmmaSmem {
   static constexpr int kWBytes = kUmmaBM * kUmmaBK * 2;  // 16 KB
   static constexpr int kXBytes = BN * kUmmaBK * 2;
-  static constexpr int kStageBytes = kWBytes + kXBytes;
-  static constexpr int kStages = (BN <= 16 ? 10 : BN <= 32 ? 9 : BN <= 64 ? 7 : BN <= 128 ? 5 : 4);
-  static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  static constexpr bool kHasA = (BN == 16);                 // decode: per-stage 16-row box of adapter A rows
+  static constexpr int kABytes = kHasA ? 16 * kUmmaBK * 2 : 0;  // 2 KB
+  static constexpr int kStageBytes = kWBytes + kXBytes + kABytes;
+  static constexpr int kStages = (BN <= 16 ? 9 : BN <= 32 ? 9 : BN <= 64 ? 7 : BN <= 128 ? 5 : 4);
+  static constexpr int kAccCols = kHasA ? 4 * BN : 2 * BN;    // [D0 D1 | V0 V1]: base + shrink accumulators
+  static constexpr int kTmemCols = (kAccCols <= 32) ? 32 : (kAccCols <= 64) ? 64 : (kAccCols <= 128) ? 128 : (kAccCols <= 256) ? 256 : 512;
   static constexpr int kBarOff = kStages * kStageBytes;
   static constexpr int kVOff = kBarOff + 256 + 5120 + 512;          // after barriers/flags, ids/leaders/shrink
   static constexpr int kVFloats = 4096;                              // 16 KB v staging (CUDA-core expand)
@@ -91,17 +104,22 @@ struct UmmaSmem {
   static constexpr int kRegion = kLoraBytes > kVFloats * 4 ? kLoraBytes : kVFloats * 4;
   static constexpr int kMetaOff = kVOff + kRegion;                  // [BN][8] ints: leader re / offB (tc expand)
   static constexpr int kBytes = kMetaOff + BN * 8 * 4 + 1024;        // + alignment slack
+  // the shrink MMA reads 128 rows (16 KB) from a stage's A box: rows 16..127 must stay inside the allocation
+  static_assert(!kHasA || kStages * (kWBytes + kXBytes) + kStages * kABytes + 16384 <= kBytes - 1024,
+                "shrink MMA window leaves the shared-memory allocation");
 };
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kUmmaThreads, 1)
     umma_lora_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                          const UmmaParams p) {
+                          const __grid_constant__ CUtensorMap tmA, const UmmaParams p) {
   using S = UmmaSmem<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sW = smem;
   uint8_t* sX = smem + S::kStages * S::kWBytes;
+  uint8_t* sA = sX + S::kStages * S::kXBytes;  // [kStages][16 x 64] adapter A rows (kHasA)
+  constexpr bool kA = S::kHasA && MODE == 0;
   uint64_t* full = (uint64_t*)(smem + S::kBarOff);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
@@ -143,6 +161,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmW);
     ptx::tma_prefetch_desc(&tmX);
+    if (kA) ptx::tma_prefetch_desc(&tmA);
     for (int s = 0; s < S::kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -214,9 +233,36 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       }
       if (nu > 0) UMMA_TRACE(2);
       if (p.pdl) ptx::pdl_wait();
+      // K-local LoRA: A rows (arena row index per slice) of the token tile's single adapter; otherwise a
+      // dummy box (row 0) keeps the pipeline uniform.  Same decision as the epilogue's (see `local`).
+      int arow[kMaxSlices] = {0, 0, 0};
+      if constexpr (kA) {
+        if (p.local && p.T <= 16 && p.g.C == 1) {
+          int a = -1;
+          bool single = true;
+          for (int t = 0; t < p.T; ++t) {
+            const int id = __ldg(p.ids + t);
+            if (id >= 0) {
+              if (a < 0) a = id;
+              else if (id != a) single = false;
+            }
+          }
+          if (single && a >= 0 && p.tab[a].rs <= 16)
+            for (int j = 0; j < p.g.J; ++j) arow[j] = (int)(p.tab[a].offA[j] / p.K);
+        }
+      }
+      auto load_a = [&](int st, int mt, int kb) {
+        if constexpr (kA) {
+          int jt = 0;
+          for (int q2 = 1; q2 < p.g.J; ++q2)
+            if (mt * kUmmaBM >= p.g.col0[q2]) jt = q2;
+          ptx::tma_load_2d(sA + st * S::kABytes, &tmA, &full[st], kb * kUmmaBK, arow[jt], pol_x);
+        }
+      };
       for (int idx = 0; idx < P; ++idx) {
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, nt = tile / M_TILES;
         ptx::tma_load_2d(sX + idx * S::kXBytes, &tmX, &full[idx], kb * kUmmaBK, nt * BN, pol_x);
+        load_a(idx, tile % M_TILES, kb);
       }
       int stage = (P == NS) ? 0 : P;
       uint32_t phase = (P == NS) ? 1u : 0u;
@@ -227,6 +273,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
         ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
         ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
+        load_a(stage, mt, kb);
         if (++stage == p.nstages) {
           stage = 0;
           phase ^= 1;
@@ -279,6 +326,13 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
 #pragma unroll
           for (int k = 0; k < kUmmaBK / 16; ++k)  // UMMA_K = 16 bf16 = 32 B -> +2 in the >>4 address field
             ptx::mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          if constexpr (kA) {  // K-local shrink: V[k][t] += A_a[k][kb] . X[t][kb] (rows >= 16 ignored)
+            const uint64_t s_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * S::kABytes));
+            const uint32_t v_tmem = tmem_base + (uint32_t)(2 * BN + acc * BN);
+#pragma unroll
+            for (int k = 0; k < kUmmaBK / 16; ++k)
+              ptx::mma_bf16(v_tmem, s_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
           ptx::mma_commit(&empty[stage]);
           if (++stage == p.nstages) {
             stage = 0;
@@ -355,10 +409,27 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         }
       }
     }
+    // K-local LoRA decision: uniform over the grid (every CTA sees the same ids; T <= 16 = one token tile)
+    // and identical to the producer's: one adapter group (or none) with r/N <= 16
+    bool local = false;
+    int la = -1;
+    if constexpr (kA) {
+      if (p.fuse && p.local && p.T <= 16 && p.g.C == 1) {
+        bool single = true;
+        for (int t = 0; t < p.T; ++t) {
+          const int id = s_fids[t];
+          if (id >= 0) {
+            if (la < 0) la = id;
+            else if (id != la) single = false;
+          }
+        }
+        local = single && (la < 0 || p.tab[la].rs <= 16);
+      }
+    }
     int cur_nt = -1;
     LoraPre pre;
     pre.a = -1;
-    if (p.fuse) {
+    if (p.fuse && !local) {
       // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
       // Units (leader token t, slice j, rank row k) are computed by the epilogue warps while the
       // producer/MMA warps stream W; a unit is computed once per DISTINCT adapter (leader = first token
@@ -466,7 +537,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       cur_nt = nt;
       if (!p.tcx) lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
     }
-    if (p.fuse) {
+    if (p.fuse && !local) {
       // every unit of the launch published before any expand reads v
       if (etid == 0) {
         UMMA_TRACE(13);
@@ -671,10 +742,15 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       for (int i = 0; i < 16; ++i) lr[i] = 0.f;
       if (!first_seg && n != pre_n) pre.a = -1;  // cached B rows belong to another output column
       pre_n = n;
-      if (!p.tcx)
+      if (local) {
+        // B rows of this thread's output column (the single adapter): gathered now, used after the stream
+        if (la >= 0 && pre.a != la) lora_pre16(pre, n, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
+      } else if (!p.tcx) {
         lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, &pre, s_v, S::kVFloats,
                      etid);
+      }
       if (first_seg && etid == 0) UMMA_TRACE(15);
+      const bool was_first = first_seg;
       first_seg = false;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
@@ -683,12 +759,47 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         UMMA_TRACE(6);
       }
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      if (local && la >= 0) {
+        // this segment's v_seg: TMEM lanes k < r/N of the shrink accumulator (warp of lane quarter 0) -> smem
+        if constexpr (kA) {
+          ptx::named_bar_sync(1, 128);  // previous readers of s_v are done
+          if (q == 0) {
+            uint32_t r2[16];
+            ptx::tmem_ld_32x32b_x16(tmem_base + (uint32_t)(2 * BN + acc * BN), r2);
+            ptx::tmem_ld_wait();
+            const int rs = p.tab[la].rs;
+            const float sc = p.tab[la].scale;
+            if (lane < rs) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) s_v[i * 16 + lane] = sc * __uint_as_float(r2[i]);
+            }
+          }
+          ptx::named_bar_sync(1, 128);
+          if (etid == 0 && was_first) UMMA_TRACE(16);
+          // lr[t] = v_seg[t] . B[:, n] for the adapter's tokens (pre.b[k] = 0 for k >= r/N)
+          if (pre.a == la) {
+            const int rs = p.tab[la].rs;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float s0 = 0.f, s1 = 0.f;
+              if (i < tv && s_ids[i] == la) {
+#pragma unroll
+                for (int k = 0; k < 16; k += 2) {
+                  s0 = fmaf(k < rs ? s_v[i * 16 + k] : 0.f, pre.b[k], s0);
+                  s1 = fmaf(k + 1 < rs ? s_v[i * 16 + k + 1] : 0.f, pre.b[k + 1], s1);
+                }
+              }
+              lr[i] = s0 + s1;
+            }
+          }
+        }
+      }
       for (int c0 = 0; c0 < tv; c0 += 16) {
         uint32_t r[16];
         ptx::tmem_ld_32x32b_x16(taddr + c0, r);
         ptx::tmem_ld_wait();
         if (whole) {
-          if (c0 > 0 && !p.tcx)
+          if (c0 > 0 && !p.tcx && !local)
             lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T,
                          &pre, s_v, S::kVFloats, etid);
           if (n < p.M) {
@@ -698,13 +809,19 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           }
         } else {
           // split tile: this CTA's fp32 partial, [row][BN] in its own slot (0 = its first segment,
-          // 1 = its last).  Columns >= tv hold exact zeros (TMA zero-fills out-of-range tokens).
+          // 1 = its last).  Columns >= tv hold exact zeros (TMA zero-fills out-of-range tokens).  K-local
+          // LoRA: the segment's LoRA share rides in the partial (c0 == 0: T <= 16).
+          float f[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]) + (local ? lr[i] : 0.f);
 #pragma unroll
           for (int i = 0; i < 16; i += 4)
-            __stcg(reinterpret_cast<float4*>(my_part + c0 + i),
-                   make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
-                               __uint_as_float(r[i + 3])));
+            __stcg(reinterpret_cast<float4*>(my_part + c0 + i), make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]));
         }
+      }
+      if (local && !whole) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) lr[i] = 0.f;  // already inside the partials: the finisher adds nothing
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
@@ -866,6 +983,17 @@ inline bool tensor_expand_enabled() {
   return env == 1;
 }
 
+// K-local LoRA for decode with few adapters (bdlora_set_decode_lora / BDLORA_LOCAL: 0 = off, 1 = auto
+// (default), 2 = always when eligible).
+inline int g_local_mode = -1;
+inline int local_lora_mode() {
+  if (g_local_mode < 0) {
+    const char* s = getenv("BDLORA_LOCAL");
+    g_local_mode = s ? std::min(2, std::max(0, atoi(s))) : 1;
+  }
+  return g_local_mode;
+}
+
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
 
 // Workspace: [sync: 3 ints, 256 B][tile counters][split-tile partials]
@@ -924,7 +1052,8 @@ inline int umma_stage_cap(int T) {
 }
 
 template <int BN, int MODE>
-inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CUtensorMap& tmX, cudaStream_t st) {
+inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
+                          cudaStream_t st) {
   using S = UmmaSmem<BN>;
   UmmaParams p1 = p0;
   p1.nstages = std::min(S::kStages, umma_stage_cap(p0.T));
@@ -945,19 +1074,19 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
   attr[0].val.programmaticStreamSerializationAllowed = p0.pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN, MODE>, tmW, tmX, p1) != cudaSuccess) return 4;
+  if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN, MODE>, tmW, tmX, tmA, p1) != cudaSuccess) return 4;
   return 0;
 }
 
 template <int MODE>
 inline int umma_dispatch_bn(int BN, const UmmaParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX,
-                            cudaStream_t st) {
+                            const CUtensorMap& tmA, cudaStream_t st) {
   switch (BN) {
-    case 16: return umma_launch_bn<16, MODE>(p, tmW, tmX, st);
-    case 32: return umma_launch_bn<32, MODE>(p, tmW, tmX, st);
-    case 64: return umma_launch_bn<64, MODE>(p, tmW, tmX, st);
-    case 128: return umma_launch_bn<128, MODE>(p, tmW, tmX, st);
-    default: return umma_launch_bn<256, MODE>(p, tmW, tmX, st);
+    case 16: return umma_launch_bn<16, MODE>(p, tmW, tmX, tmA, st);
+    case 32: return umma_launch_bn<32, MODE>(p, tmW, tmX, tmA, st);
+    case 64: return umma_launch_bn<64, MODE>(p, tmW, tmX, tmA, st);
+    case 128: return umma_launch_bn<128, MODE>(p, tmW, tmX, tmA, st);
+    default: return umma_launch_bn<256, MODE>(p, tmW, tmX, tmA, st);
   }
 }
 
@@ -965,7 +1094,7 @@ inline int umma_dispatch_bn(int BN, const UmmaParams& p, const CUtensorMap& tmW,
 inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_bfloat16* W, const int* ids,
                        const SlotEntry* tab, const __nv_bfloat16* arena, const float* v, __nv_bfloat16* Y, void* ws,
                        int num_sms, cudaStream_t st, int pdl = 0, float* v_fused = nullptr, int rs_max = 0,
-                       int tcx = 0) {
+                       int tcx = 0, const CUtensorMap* amap = nullptr) {
   if (!umma_eligible(g, T)) return 1;
   if (v_fused && T > kFuseMaxT) return 1;
   const int BN = umma_bn_for(T);
@@ -1012,12 +1141,17 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   if (v_fused) p.v = v_fused;
   p.pdl = pdl;
   p.trace = g_umma_trace;
+  // K-local LoRA needs the arena's A-row tensor map and tiles that never straddle a slice boundary
+  bool aligned = true;
+  for (int j = 1; j < g.J; ++j) aligned = aligned && (g.col0[j] % kUmmaBM == 0);
+  p.local = (v_fused && amap && aligned && BN == 16) ? local_lora_mode() : 0;
   p.nstages = 0;  // set per BN
   p.route = nullptr;
   CUtensorMap tmW, tmX;
   if (!encode_kmajor(&tmW, W, p.K, p.M, kUmmaBM)) return 3;
   if (!encode_kmajor(&tmX, X, p.K, p.T, BN)) return 3;
-  return umma_dispatch_bn<0>(BN, p, tmW, tmX, st);
+  // without K-local LoRA the A boxes are dummies (row 0 of the arena map, or of X): same bytes, ignored
+  return umma_dispatch_bn<0>(BN, p, tmW, tmX, amap ? *amap : tmX, st);
 }
 
 // Tensor-core shrink: v[t][j][k] = s_a X[t] . A_{a,j}[k] for every token t of every distinct adapter a,
@@ -1055,13 +1189,14 @@ inline int umma_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, cons
   p.X = X;
   p.fuse = 0;
   p.tcx = 0;
+  p.local = 0;
   p.v_out = v_out;
   p.route = route;
   p.pdl = pdl;
   p.trace = g_umma_trace;
   CUtensorMap tmX;
   if (!encode_kmajor(&tmX, X, p.K, p.T, BN)) return 3;
-  return umma_dispatch_bn<1>(BN, p, amap, tmX, st);
+  return umma_dispatch_bn<1>(BN, p, amap, tmX, amap, st);
 }
 
 }  // namespace bdl

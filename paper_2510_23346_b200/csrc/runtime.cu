@@ -301,7 +301,7 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, T, (const __nv_bfloat16*)W, ids, p->d_tab,
                               (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
-                              p->num_sms, st, pdl, nullptr, 0, /*tcx=*/1);
+                              p->num_sms, st, pdl, nullptr, 0, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
     if (rc == 0) {
       count_launch();
       CU_TRY(cudaGetLastError());
@@ -341,6 +341,12 @@ int bdlora_abi_version(void) { return BDLORA_ABI_VERSION; }
 
 int bdlora_set_pdl(int enable) {
   g_pdl = enable ? 1 : 0;
+  return BDLORA_OK;
+}
+
+int bdlora_set_decode_lora(int mode) {
+  if (mode < 0 || mode > 2) return fail(BDLORA_E_ARG, "bdlora_set_decode_lora: mode %d not in {0, 1, 2}", mode);
+  bdl::g_local_mode = mode;
   return BDLORA_OK;
 }
 
@@ -792,11 +798,12 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
                     cudaStream_t st) {
   float* v = ws_v(p, ws, T);
   if (bdl::umma_eligible(p->g, (int)T) && T < kTcShrinkMinT) {
-    // decode: ONE kernel -- the shrink runs in the GEMM's epilogue warps while the weights stream
+    // decode: ONE kernel -- the LoRA shrink runs inside it (K-local on the tensor cores for a single
+    // adapter group, else in the epilogue warps) while the weights stream
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, (int)T, (const __nv_bfloat16*)W, ids, p->d_tab,
                               (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
-                              p->num_sms, st, g_pdl, v, p->rs_max);
+                              p->num_sms, st, g_pdl, v, p->rs_max, 0, p->amap_ok ? &p->amap : nullptr);
     if (rc == 0) {
       count_launch();
       CU_TRY(cudaGetLastError());

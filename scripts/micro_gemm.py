@@ -52,8 +52,10 @@ def run(M, K, T, lora=True, rank=16):
     us_fwd = bench(lambda i: bd.bdlora_column_forward(pool, X, Ws[i % nrep], ids, Y, ws), nrep)
     us_sh = bench(lambda i: bd.bdlora_lora_shrink(pool, X, ids, v, ws), nrep)
     us_cublas = bench(lambda i: torch.matmul(X, Ws[i % nrep].t()), nrep)
+    nids = -torch.ones(T, dtype=torch.int32, device=dev)
+    us_base = bench(lambda i: bd.bdlora_column_forward(pool, X, Ws[i % nrep], nids, Y, ws), nrep)
     gb = (M * K * 2) / 1e9
-    out = dict(M=M, K=K, T=T, lora=lora, us_gemm=us, us_fwd=us_fwd, us_shrink=us_sh, us_cublas=us_cublas,
+    out = dict(M=M, K=K, T=T, lora=lora, us_gemm=us, us_fwd=us_fwd, us_shrink=us_sh, us_cublas=us_cublas, us_fwd_nolora=us_base,
                gbs_gemm=gb / (us * 1e-6), gbs_cublas=gb / (us_cublas * 1e-6))
     pool.close()
     return out
@@ -61,10 +63,9 @@ def run(M, K, T, lora=True, rank=16):
 
 if __name__ == "__main__":
     res = []
-    shapes = [(1024, 4096), (2048, 4096), (4096, 4096), (6144, 4096), (14336, 4096), (28672, 4096), (4096, 14336),
-              (768, 4096), (512, 4096), (4096, 512), (4096, 1792)]
+    shapes = [(4096, 4096), (6144, 4096), (28672, 4096), (4096, 14336), (768, 4096), (4096, 512), (4096, 1792)]
     for M, K in shapes:
-        for T in (1, 16):
+        for T in (1,):
             r = run(M, K, T)
             res.append(r)
             print(json.dumps(r), flush=True)

@@ -24,7 +24,7 @@ Y = torch.empty(T, M, dtype=torch.bfloat16, device=dev)
 ws = bd.make_workspace(pool, T)
 v = torch.zeros(bd.bdlora_v_elems(pool, T), dtype=torch.float32, device=dev)
 bd.bdlora_lora_shrink(pool, X, ids, v, ws)
-tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
+tr = torch.zeros(148 * 32, dtype=torch.int64, device=dev)
 for i in range(6):
     bd.bdlora_base_expand(pool, X, Ws[i % nrep], ids, v, Y, ws)
 torch.cuda.synchronize()
@@ -32,24 +32,28 @@ fused = len(sys.argv) > 4 and sys.argv[4] == "fused"
 shrink_only = len(sys.argv) > 4 and sys.argv[4] == "shrink"
 bd.bdlora_debug_trace(tr)
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-s.record()
-if fused:
-    bd.bdlora_column_forward(pool, X, Ws[0], ids, Y, ws)
-elif shrink_only:
+for rep in range(3):
+  s.record()
+  if fused:
+    bd.bdlora_column_forward(pool, X, Ws[rep % nrep], ids, Y, ws)
+  elif shrink_only:
     bd.bdlora_lora_shrink(pool, X, ids, v, ws)
-else:
-    bd.bdlora_base_expand(pool, X, Ws[0], ids, v, Y, ws)
-e.record()
-torch.cuda.synchronize()
+  else:
+    bd.bdlora_base_expand(pool, X, Ws[rep % nrep], ids, v, Y, ws)
+  e.record()
+  torch.cuda.synchronize()
 bd.bdlora_debug_trace(None)
-t = tr.view(148, 16).cpu().numpy().astype("int64")
+t = tr.view(148, 32).cpu().numpy().astype("int64")
 used = t[:, 0] > 0
 t = t[used]
 t0 = t[:, 0].min()
 names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit", "fin_beg",
-         "fin_end", "arrived", "part_beg", "shr_done", "v_ready", "lora1"]
+         "fin_end", "arrived", "part_beg", "shr_done", "v_ready", "lora1",
+         "probe0", "pre_b", "v_ld", "probe_bar"]
 print(f"M={M} K={K} T={T} event time {s.elapsed_time(e)*1e3:.1f} us, CTAs {used.sum()}")
 for k, nm in enumerate(names):
+    if (t[:, k] <= 0).all():
+        continue
     col = (t[:, k] - t0) / 1e3
     print(f"{nm:10s} min {col.min():7.2f}  med {sorted(col)[len(col)//2]:7.2f}  max {col.max():7.2f} us")
 order = (t[:, 8] - t0).argsort()[::-1][:6]

@@ -401,6 +401,52 @@ def test_pdl_on_off_identical(dev, pdl):
     _assert_tol(_np(y), ol.column_device_output(ref_full, 8, 3), f"pdl={pdl}")
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("pi,n,T", [(0, 1, 1), (0, 8, 5), (2, 1, 16), (2, 4, 3), (3, 2, 7), (1, 1, 1), (3, 8, 12)])
+def test_decode_lora_schedules(dev, mode, pi, n, T):
+    """Decode (T <= 16) single-kernel forward under the three LoRA schedules of bdlora_set_decode_lora
+    (0 global shrink, 1 auto, 2 K-local: each K-range contributor adds s (X_seg A_seg) B to its partial,
+    Alg. 1/2 regrouped over K) -- all against the oracle.  8B shapes: QKV whole/split-K tiles, gate_up
+    stream-K, O and down row partials (split-K)."""
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.arch_projections("llama-3.1-8b")[pi]
+    case = H.make_case(900 + 31 * pi + 7 * n + T, proj, "bd", n, T, ranks=[16, 32, 8])
+    ads = case.oracle_adapters()
+    bd.bdlora_set_decode_lora(mode)
+    try:
+        for i in sorted({0, n - 1}):
+            if proj.parallel == "column":
+                ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, ads, case.ids, "bd", n)
+                _assert_tol(_np(run_column(case, i, dev)), ol.column_device_output(ref_full, n, i),
+                            f"mode={mode} rank {i}")
+            else:
+                _assert_tol(_np(run_row_partial(case, i, dev)),
+                            ol.row_partial_bd(case.X.f64, case.W.f64, ads, case.ids, n, i), f"mode={mode} rank {i}")
+    finally:
+        bd.bdlora_set_decode_lora(1)
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+@pytest.mark.parametrize("n", [1, 4])
+def test_integer_mode_bit_exact_decode(dev, mode, n):
+    """P10 at decode sizes (T <= 16, single-kernel forward) under the global and the K-local LoRA
+    schedule: bit-identical to the oracle rounded once to bf16 on every rank."""
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.Projection("qkv", "column", 1024, (512, 256, 256))
+    case = H.make_case(700 + n, proj, "bd", n, 9, ranks=[8, 16, 8, 32], integer=True)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", n)
+    bd.bdlora_set_decode_lora(mode)
+    try:
+        for i in range(n):
+            ref = ol.bf16_round(ol.column_device_output(ref_full, n, i))
+            got = _np(run_column(case, i, dev))
+            assert np.array_equal(got, ref), f"mode={mode} rank {i}: {np.count_nonzero(got != ref)} mismatches"
+    finally:
+        bd.bdlora_set_decode_lora(1)
+
+
 def test_cuda_core_gemv_path_k_not_multiple_of_64(dev):
     """K % 64 != 0 takes the CUDA-core GEMV kernel (still on the GPU): parity on a ragged K."""
     proj = synth.Projection("odd", "column", 200, (96, 32))
