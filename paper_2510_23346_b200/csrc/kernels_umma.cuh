@@ -23,6 +23,7 @@
 #include "ptx.cuh"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 namespace bdl {
@@ -55,6 +56,8 @@ struct UmmaParams {
   int* sync;         // fused mode: [0] unit claim counter, [1] units done, [2] CTAs exited (zero between launches)
   long long* trace;  // optional per-CTA timestamps (ns, %globaltimer) for profiling; nullptr = off
   int local;         // fused mode: 0 = global shrink, 1 = K-local LoRA when the tile's adapters are few, 2 = always
+  int cluster;       // > 1: launched with clusters of `cluster` split-K contributors of ONE tile (plain split-K
+                     // grid, cluster = s); partials reduced through distributed shared memory, no global fix-up
 };
 
 // K-local LoRA (decode, one adapter group per token tile).  The layer is linear in a partition of K:
@@ -103,7 +106,11 @@ struct UmmaSmem {
   static constexpr int kLoraBytes = kLoraA + 2 * kLoraV;
   static constexpr int kRegion = kLoraBytes > kVFloats * 4 ? kLoraBytes : kVFloats * 4;
   static constexpr int kMetaOff = kVOff + kRegion;                  // [BN][8] ints: leader re / offB (tc expand)
-  static constexpr int kBytes = kMetaOff + BN * 8 * 4 + 1024;        // + alignment slack
+  // cluster split-K (decode): [s][ceil(128/s)][BN] fp32 partial slots pushed by the peers (dedicated: a peer
+  // may push while this CTA still streams)
+  static constexpr int kPartOff = kMetaOff + BN * 8 * 4;
+  static constexpr int kPartBytes = kHasA ? (kUmmaBM + 8) * BN * 4 : 0;
+  static constexpr int kBytes = kPartOff + kPartBytes + 1024;        // + alignment slack
   // the shrink MMA reads 128 rows (16 KB) from a stage's A box: rows 16..127 must stay inside the allocation
   static_assert(!kHasA || kStages * (kWBytes + kXBytes) + kStages * kABytes + 16384 <= kBytes - 1024,
                 "shrink MMA window leaves the shared-memory allocation");
@@ -138,6 +145,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_pcol = s_misc + 16;                     // [8][6] tensor-core expand pass columns (a, j, k0, re, boff lo/hi)
   int* s_gmeta = (int*)(smem + S::kMetaOff);     // [BN][8] per leader token: re, offB[0..2] (lo, hi)
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
+  float* s_preb = s_v + 256;                     // K-local mode: [16][128] B rows of each thread's column
+  float* s_part = (float*)(smem + S::kPartOff);  // cluster split-K partial slots
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -376,6 +385,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..127
+    const int crank = p.cluster > 1 ? (int)ptx::cluster_ctarank() : 0;
     if (p.pdl) ptx::pdl_wait();         // the preceding kernel is complete and visible (X, ids, and v
                                         // when it was a shrink); also orders our Y writes after it
     if (p.fuse && etid == 0) s_misc[0] = atomicAdd(p.sync + 0, 1);  // fused-shrink arrival ticket (below)
@@ -426,6 +436,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         local = single && (la < 0 || p.tab[la].rs <= 16);
       }
     }
+    const int la_rs = (local && la >= 0) ? p.tab[la].rs : 0;  // loaded once, early (off the tail)
+    const float la_sc = (local && la >= 0) ? p.tab[la].scale : 0.f;
     int cur_nt = -1;
     LoraPre pre;
     pre.a = -1;
@@ -437,12 +449,16 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const int Js = p.g.J, rsm = p.rs_max;
       const int U_s = p.T * Js * rsm;
       const int warp_e = etid >> 5;
-      // units are owned by ARRIVAL TICKET: a CTA draws its ticket once it runs, so every unit belongs to a
-      // resident CTA (no deadlock whatever the residency) and costs one atomic per CTA, not per unit
+      // units are claimed in batches b = {b, b + G, b + 2G, ...} (G = gridDim.x): a CTA's first batch is its
+      // arrival ticket (one atomic per CTA when every CTA is resident); whoever finishes a batch claims the next
+      // unclaimed one, so every unit is computed by a RESIDENT CTA whatever the residency (clusters may not
+      // all fit in one wave) -- no CTA can wait for v that a not-yet-resident CTA owns
       ptx::named_bar_sync(1, 128);
-      const int ticket = s_misc[0];
+      int batch = s_misc[0];
       int mine = 0;
-      for (int us = ticket; us < U_s; us += (int)gridDim.x) {
+      const int n_batches = min((int)gridDim.x, U_s);
+      while (batch < n_batches) {
+      for (int us = batch; us < U_s; us += (int)gridDim.x) {
         ++mine;
         const int t_lead = us / (Js * rsm), j = (us / rsm) % Js, k = us % rsm;
         const int a = s_fids[t_lead];
@@ -496,6 +512,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           }
         }
       }
+        ptx::named_bar_sync(1, 128);  // s_misc / s_mem of this batch no longer read
+        if (etid == 0) s_misc[0] = atomicAdd(p.sync + 0, 1);
+        ptx::named_bar_sync(1, 128);
+        batch = s_misc[0];
+      }
       ptx::named_bar_sync(1, 128);
       if (etid == 0 && mine) ptx::atom_add_acq_rel_gpu(p.sync + 1, mine);  // publishes my v (release)
     }
@@ -536,6 +557,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       ptx::named_bar_sync(1, 128);
       cur_nt = nt;
       if (!p.tcx) lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
+      if (local && pre.a >= 0) {  // park the gathered B rows in smem now: the loads complete during the stream
+#pragma unroll
+        for (int q2 = 0; q2 < 16; ++q2) s_preb[q2 * 128 + etid] = pre.b[q2];
+      }
     }
     if (p.fuse && !local) {
       // every unit of the launch published before any expand reads v
@@ -744,7 +769,13 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       pre_n = n;
       if (local) {
         // B rows of this thread's output column (the single adapter): gathered now, used after the stream
-        if (la >= 0 && pre.a != la) lora_pre16(pre, n, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
+        if (la >= 0 && pre.a != la) {
+          lora_pre16(pre, n, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
+          if (pre.a >= 0) {
+#pragma unroll
+            for (int q2 = 0; q2 < 16; ++q2) s_preb[q2 * 128 + etid] = pre.b[q2];
+          }
+        }
       } else if (!p.tcx) {
         lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, &pre, s_v, S::kVFloats,
                      etid);
@@ -767,31 +798,30 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             uint32_t r2[16];
             ptx::tmem_ld_32x32b_x16(tmem_base + (uint32_t)(2 * BN + acc * BN), r2);
             ptx::tmem_ld_wait();
-            const int rs = p.tab[la].rs;
-            const float sc = p.tab[la].scale;
-            if (lane < rs) {
+            if (lane < la_rs) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) s_v[i * 16 + lane] = sc * __uint_as_float(r2[i]);
+              for (int i = 0; i < 16; ++i) s_v[i * 16 + lane] = la_sc * __uint_as_float(r2[i]);
             }
           }
           ptx::named_bar_sync(1, 128);
           if (etid == 0 && was_first) UMMA_TRACE(16);
           // lr[t] = v_seg[t] . B[:, n] for the adapter's tokens (pre.b[k] = 0 for k >= r/N)
           if (pre.a == la) {
-            const int rs = p.tab[la].rs;
+            const int rs = la_rs;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               float s0 = 0.f, s1 = 0.f;
               if (i < tv && s_ids[i] == la) {
 #pragma unroll
                 for (int k = 0; k < 16; k += 2) {
-                  s0 = fmaf(k < rs ? s_v[i * 16 + k] : 0.f, pre.b[k], s0);
-                  s1 = fmaf(k + 1 < rs ? s_v[i * 16 + k + 1] : 0.f, pre.b[k + 1], s1);
+                  s0 = fmaf(k < rs ? s_v[i * 16 + k] : 0.f, s_preb[k * 128 + etid], s0);
+                  s1 = fmaf(k + 1 < rs ? s_v[i * 16 + k + 1] : 0.f, s_preb[(k + 1) * 128 + etid], s1);
                 }
               }
               lr[i] = s0 + s1;
             }
           }
+          if (etid == 0 && was_first) UMMA_TRACE(17);
         }
       }
       for (int c0 = 0; c0 < tv; c0 += 16) {
@@ -812,11 +842,27 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           // 1 = its last).  Columns >= tv hold exact zeros (TMA zero-fills out-of-range tokens).  K-local
           // LoRA: the segment's LoRA share rides in the partial (c0 == 0: T <= 16).
           float f[16];
+          if (p.cluster > 1 && !local && !p.tcx && crank == 0 && c0 > 0)  // rank 0 carries the LoRA term
+            lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T,
+                         &pre, s_v, S::kVFloats, etid);
+          const bool add_lr = local || (p.cluster > 1 && !p.tcx && crank == 0);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]) + (local ? lr[i] : 0.f);
+          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]) + (add_lr ? lr[i] : 0.f);
+          if (p.cluster > 1) {
+            // pushed into the OWNER rank's shared memory (DSMEM stores, no round trip): owner c of rows
+            // [c*128/s, (c+1)*128/s) keeps [s][ceil(128/s)][BN] fp32 slots in its idle ring
+            const int s = p.cluster, nr_max = (kUmmaBM + s - 1) / s;
+            const int owner = ((row + 1) * s - 1) / kUmmaBM;
+            const int rr = row - (owner * kUmmaBM) / s;
+            const uint32_t dst =
+                ptx::mapa(ptx::smem_u32(s_part + ((size_t)(crank * nr_max + rr) * BN + c0)), (uint32_t)owner);
 #pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            __stcg(reinterpret_cast<float4*>(my_part + c0 + i), make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]));
+            for (int i = 0; i < 16; i += 4) ptx::st_dsmem_f4(dst + i * 4, f[i], f[i + 1], f[i + 2], f[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+              __stcg(reinterpret_cast<float4*>(my_part + c0 + i), make_float4(f[i], f[i + 1], f[i + 2], f[i + 3]));
+          }
         }
       }
       if (local && !whole) {
@@ -825,7 +871,34 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       }
       ptx::tc_fence_before();
       ptx::mbar_arrive(&tempty[acc]);
-      if (!whole) {
+      if (!whole && p.cluster > 1) {
+        // cluster split-K: the tile's s contributors are this cluster; rank c sums rows [c*128/s, (c+1)*128/s)
+        // of every peer's partial (DSMEM, rank order -> deterministic), rounds once, stores Y
+        if (etid == 0) UMMA_TRACE(12);
+        ptx::cluster_arrive();  // release: my DSMEM stores -> the owners
+        ptx::cluster_wait();    // acquire: every peer's rows of my range are in my shared memory
+        if (etid == 0) UMMA_TRACE(11);
+        const int s = p.cluster, nr_max = (kUmmaBM + s - 1) / s;
+        const int r_lo = (crank * kUmmaBM) / s, r_hi = ((crank + 1) * kUmmaBM) / s, nr = r_hi - r_lo;
+        const int nq = (tv + 3) / 4;
+        const float* sp = s_part;
+        for (int f = etid; f < nr * nq; f += 128) {
+          const int rr = f % nr, qd = f / nr;
+          float4 y = *reinterpret_cast<const float4*>(sp + (size_t)rr * BN + qd * 4);
+          for (int c = 1; c < s; ++c) {  // contributors in rank order: deterministic
+            const float4 z = *reinterpret_cast<const float4*>(sp + ((size_t)(c * nr_max + rr) * BN + qd * 4));
+            y.x += z.x, y.y += z.y, y.z += z.z, y.w += z.w;
+          }
+          const int nn = mt * kUmmaBM + r_lo + rr;
+          if (nn < p.M) {
+            const float yv[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (qd * 4 + i < tv) p.Y[(size_t)(t0 + qd * 4 + i) * p.M + nn] = __float2bfloat16_rn(yv[i]);
+          }
+        }
+        if (etid == 0) UMMA_TRACE(10);
+      } else if (!whole) {
         if (etid == 0) UMMA_TRACE(12);
         // arrival: CTA barrier, then ONE thread publishes with a gpu-scope acq_rel atomic (the
         // barrier + cumulative fence order every thread's partial before it)
@@ -954,6 +1027,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
   }
 
+  if (MODE == 0 && p.cluster > 1 && warp < 2) {  // the epilogue's cluster barrier counts every thread
+    ptx::cluster_arrive();
+    ptx::cluster_wait();
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -992,6 +1069,16 @@ inline int local_lora_mode() {
     g_local_mode = s ? std::min(2, std::max(0, atoi(s))) : 1;
   }
   return g_local_mode;
+}
+
+// Split-K partial reduction through thread-block-cluster DSMEM (BDLORA_CLUSTER=0 disables: global fix-up).
+inline int g_cluster_mode = -1;
+inline bool cluster_splitk_enabled() {
+  if (g_cluster_mode < 0) {
+    const char* s = getenv("BDLORA_CLUSTER");
+    g_cluster_mode = (s && s[0] == '0') ? 0 : 1;
+  }
+  return g_cluster_mode == 1;
 }
 
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
@@ -1057,6 +1144,35 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
   using S = UmmaSmem<BN>;
   UmmaParams p1 = p0;
   p1.nstages = std::min(S::kStages, umma_stage_cap(p0.T));
+  if (MODE == 0 && p1.cluster > 1) {
+    // every cluster must be co-resident in one wave (one CTA per SM); otherwise the global fix-up
+    static int max_clusters[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+    int& mc = max_clusters[p1.cluster];
+    if (mc < 0) {
+      if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               S::kBytes) != cudaSuccess)
+        return 2;
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3(p0.grid);
+      qc.blockDim = dim3(kUmmaThreads);
+      qc.dynamicSmemBytes = S::kBytes;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = p1.cluster;
+      ca[0].val.clusterDim.y = 1;
+      ca[0].val.clusterDim.z = 1;
+      qc.attrs = ca;
+      qc.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&mc, (void*)umma_lora_gemm_kernel<BN, MODE>, &qc) != cudaSuccess) {
+        cudaGetLastError();
+        mc = 0;
+      }
+    }
+    if ((long long)mc * p1.cluster < p0.grid) p1.cluster = 1;
+    if (getenv("BDLORA_DEBUG"))
+      fprintf(stderr, "[bdlora] umma BN=%d grid=%d cluster=%d (max active clusters %d) -> %d\n", BN, p0.grid,
+              p0.cluster, mc, p1.cluster);
+  }
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1069,11 +1185,18 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
   cfg.blockDim = dim3(kUmmaThreads);
   cfg.dynamicSmemBytes = S::kBytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = p0.pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (MODE == 0 && p1.cluster > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = p1.cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
+  }
   if (cudaLaunchKernelEx(&cfg, umma_lora_gemm_kernel<BN, MODE>, tmW, tmX, tmA, p1) != cudaSuccess) return 4;
   return 0;
 }
@@ -1113,8 +1236,15 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   // tiles > #SM: stream-K over all SMs.  Both keep >= 8 k-blocks per CTA so a split tile has few
   // contributors.  (The stream-K formula with grid = tiles * s reproduces the split-K ranges.)
   const long long tiles = (long long)p.m_tiles * p.n_tiles;
+  p.cluster = 1;
   if (tiles <= num_sms) {
     long long s = std::max<long long>(1, std::min<long long>(num_sms / tiles, p.k_blocks / 8));
+    // cluster split-K (the s contributors of a tile reduce through DSMEM): cheap fix-up, so split finer
+    const long long sc = std::min<long long>(8, std::min<long long>(num_sms / tiles, p.k_blocks / 4));
+    if (cluster_splitk_enabled() && BN == 16 && sc >= 2) {
+      s = sc;
+      p.cluster = (int)sc;
+    }
     p.grid = (int)(tiles * s);
   } else if (BN >= 128) {
     // compute-bound token tiles (prefill): one whole tile per CTA, no split fix-ups (a split 128 x 256
