@@ -118,8 +118,10 @@ __device__ __forceinline__ float lora_expand_term(int t, int n, int a, const Slo
 // B rows of ONE adapter gathered ahead of time (decode fast path: the first 16-token chunk holds a single
 // adapter group, C == 1, re <= 16) so only the v load remains once v is ready.
 struct LoraPre {
-  int a;  // adapter id, -1 = none
-  float b[16];
+  int a;            // adapter id, -1 = none
+  int re;           // its expand rank (<= 16): with b, everything the expand needs -- no slot-table read later
+  float b[16];      // the B rows (registers) -- unused when sb is set
+  float* sb;        // optional shared-memory home of the B rows (sb[q * 128]): nothing long-lived in registers
 };
 
 __device__ __forceinline__ void lora_pre16(LoraPre& pre, int n, int cnt, const int* s_ids, const int* s_lead,
@@ -144,16 +146,23 @@ __device__ __forceinline__ void lora_pre16(LoraPre& pre, int n, int cnt, const i
   if (re > 16) return;
   const int ldb = g.e_hi[j] - g.e_lo[j];
   const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + tab[a].offB[j]) + (n - g.e_lo[j]);
+  if (pre.sb) {
 #pragma unroll
-  for (int q = 0; q < 16; ++q) pre.b[q] = (q < re) ? bf16_bits_to_f32(__ldg(B + (size_t)q * ldb)) : 0.f;
+    for (int q = 0; q < 16; ++q) pre.sb[q * 128] = (q < re) ? bf16_bits_to_f32(__ldg(B + (size_t)q * ldb)) : 0.f;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) pre.b[q] = (q < re) ? bf16_bits_to_f32(__ldg(B + (size_t)q * ldb)) : 0.f;
+  }
   pre.a = a;
+  pre.re = re;
 }
 
 __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int cnt, const int* s_ids,
                                              const int* s_lead, const SlotEntry* __restrict__ tab,
                                              const __nv_bfloat16* __restrict__ arena, const Geom& g,
                                              const float* __restrict__ v, int T, LoraPre* pre = nullptr,
-                                             float* s_v = nullptr, int s_v_cap = 0, int etid = 0) {
+                                             float* s_v = nullptr, int s_v_cap = 0, int etid = 0,
+                                             long long* trace = nullptr) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) lr[i] = 0.f;
   // Stage this chunk's v rows in shared memory (cooperatively, once) when they fit: the inner loop then
@@ -162,14 +171,33 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
   const bool staged = s_v != nullptr && g.C * 16 * per_tok <= s_v_cap;
   if (staged) {
     asm volatile("bar.sync 1, 128;" ::: "memory");  // previous readers of s_v are done
+    if (trace && etid == 0) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[18] = t;
+    }
     for (int c = 0; c < g.C; ++c) {
       const float* src = v + (size_t)(c * T + tb) * per_tok;
       float* dst = s_v + (size_t)c * 16 * per_tok;
       for (int idx = etid; idx < cnt * per_tok; idx += 128) dst[idx] = __ldg(src + idx);
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (trace && etid == 0) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[19] = t;
+    }
+#define LC_STAMP(k)                                                    \
+  do {                                                                 \
+    if (trace && etid == 0) {                                          \
+      long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory"); \
+      trace[k] = t_;                                                   \
+    }                                                                  \
+  } while (0)
   }
   if (n >= g.M) return;
+  LC_STAMP(20);
   int j = 0;
 #pragma unroll
   for (int q = 1; q < kMaxSlices; ++q)
@@ -178,6 +206,7 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
   const int ldb = g.e_hi[j] - g.e_lo[j];
   const int col = n - g.e_lo[j];
   const unsigned full = (cnt >= 16) ? 0xffffu : ((1u << cnt) - 1u);
+  LC_STAMP(21);
   for (int i = 0; i < cnt; ++i) {
     if (s_lead[i] != i) continue;  // not a group leader (or no adapter)
     const int a = s_ids[i];
@@ -185,25 +214,51 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
 #pragma unroll
     for (int i2 = 0; i2 < 16; ++i2)
       if (i2 < cnt && s_lead[i2] == i) mask |= 1u << i2;
-    const uint16_t* B = reinterpret_cast<const uint16_t*>(arena + tab[a].offB[j]) + col;
-    const int rc = tab[a].re / g.C;
+    LC_STAMP(22);
+    const bool use_pre = pre && pre->a == a;  // pre-gathered (C == 1, re <= 16): no slot-table round trip
+    const uint16_t* B = use_pre ? nullptr : reinterpret_cast<const uint16_t*>(arena + tab[a].offB[j]) + col;
+    const int rc = use_pre ? pre->re : tab[a].re / g.C;
     for (int c = 0; c < g.C; ++c) {
       for (int k0 = 0; k0 < rc; k0 += 16) {
         float b[16];
-        if (pre && pre->a == a && c == 0 && k0 == 0) {
+        if (use_pre && c == 0 && k0 == 0) {
+          if (pre->sb) {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) b[q] = pre->b[q];
+            for (int q = 0; q < 16; ++q) b[q] = pre->sb[q * 128];
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) b[q] = pre->b[q];
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < 16; ++q)
             b[q] = (k0 + q < rc) ? bf16_bits_to_f32(__ldg(B + (size_t)(c * rc + k0 + q) * ldb)) : 0.f;
           if (pre && g.C == 1 && rc <= 16) {  // keep for the next chunk of the same tile (same adapter)
             pre->a = a;
+            pre->re = rc;
+            if (pre->sb) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) pre->b[q] = b[q];
+              for (int q = 0; q < 16; ++q) pre->sb[q * 128] = b[q];
+            } else {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) pre->b[q] = b[q];
+            }
           }
         }
         const bool vec = staged && (g.Rc & 3) == 0 && k0 + 16 <= rc;
+        if (staged && cnt == 1 && mask == 1u) {
+          // decode batch 1: one dot product (masked to the rank), small code on the critical tail
+          const float* vv = s_v + ((size_t)(c * 16) * g.J + j) * g.Rc + k0;
+          float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) {
+            s0 = fmaf(k0 + q < rc ? vv[q] : 0.f, b[q], s0);
+            s1 = fmaf(k0 + q + 1 < rc ? vv[q + 1] : 0.f, b[q + 1], s1);
+          }
+          lr[0] += s0 + s1;
+          LC_STAMP(23);
+          continue;
+        }
         if (vec && mask == full) {
           // one adapter for the whole chunk: branch-free, every LDS.128 independent (pipelined)
 #pragma unroll
@@ -220,6 +275,7 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
             }
             if (i2 < cnt) lr[i2] += (s0 + s1) + (s2 + s3);
           }
+          LC_STAMP(23);
           continue;
         }
 #pragma unroll

@@ -110,8 +110,11 @@ struct UmmaSmem {
   // may push while this CTA still streams)
   static constexpr int kPartOff = kMetaOff + BN * 8 * 4;
   static constexpr int kPartBytes = kHasA ? (kUmmaBM + 8) * BN * 4 : 0;
-  static constexpr int kBytes = kPartOff + kPartBytes + 1024;        // + alignment slack
+  static constexpr int kPreBOff = kPartOff + kPartBytes;              // [16][128] fp32 pre-gathered B rows
+  static constexpr int kPreBBytes = kHasA ? 16 * 128 * 4 : 0;
+  static constexpr int kBytes = kPreBOff + kPreBBytes + 1024;        // + alignment slack
   // the shrink MMA reads 128 rows (16 KB) from a stage's A box: rows 16..127 must stay inside the allocation
+  static_assert(kBytes <= 232448, "exceeds 227 KB of dynamic shared memory per CTA");
   static_assert(!kHasA || kStages * (kWBytes + kXBytes) + kStages * kABytes + 16384 <= kBytes - 1024,
                 "shrink MMA window leaves the shared-memory allocation");
 };
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_pcol = s_misc + 16;                     // [8][6] tensor-core expand pass columns (a, j, k0, re, boff lo/hi)
   int* s_gmeta = (int*)(smem + S::kMetaOff);     // [BN][8] per leader token: re, offB[0..2] (lo, hi)
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
-  float* s_preb = s_v + 256;                     // K-local mode: [16][128] B rows of each thread's column
+  float* s_preb = (float*)(smem + S::kPreBOff);  // decode: [16][128] B rows of each thread's column (parked)
   float* s_part = (float*)(smem + S::kPartOff);  // cluster split-K partial slots
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -235,16 +238,18 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const int nu = u_hi - u_lo;
       const int NS = p.nstages;
       const int P = min(nu, NS);
-      for (int idx = 0; idx < P; ++idx) {
+      for (int idx = 0; idx < P; ++idx) {  // expect (no arrival yet): the stage cannot complete before X/A
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, mt = tile % M_TILES;
-        ptx::mbar_arrive_expect_tx(&full[idx], S::kStageBytes);
+        ptx::mbar_expect_tx(&full[idx], S::kWBytes);
         ptx::tma_load_2d(sW + idx * S::kWBytes, &tmW, &full[idx], kb * kUmmaBK, mt * kUmmaBM, pol_w);
       }
       if (nu > 0) UMMA_TRACE(2);
       if (p.pdl) ptx::pdl_wait();
-      // K-local LoRA: A rows (arena row index per slice) of the token tile's single adapter; otherwise a
-      // dummy box (row 0) keeps the pipeline uniform.  Same decision as the epilogue's (see `local`).
+      // K-local LoRA: A rows (arena row index per slice) of the token tile's single adapter, loaded only when
+      // the K-local schedule is taken (same decision as the epilogue's, see `local`; the MMA warp reads it
+      // from s_misc[8], written before the first arrival on full[0])
       int arow[kMaxSlices] = {0, 0, 0};
+      bool use_a = false;
       if constexpr (kA) {
         if (p.local && p.T <= 16 && p.g.C == 1) {
           int a = -1;
@@ -256,12 +261,16 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               else if (id != a) single = false;
             }
           }
-          if (single && a >= 0 && p.tab[a].rs <= 16)
+          if (single && a >= 0 && p.tab[a].rs <= 16) {
+            use_a = true;
             for (int j = 0; j < p.g.J; ++j) arow[j] = (int)(p.tab[a].offA[j] / p.K);
+          }
         }
       }
+      s_misc[8] = use_a ? 1 : 0;
+      const uint32_t a_bytes = use_a ? (uint32_t)S::kABytes : 0u;
       auto load_a = [&](int st, int mt, int kb) {
-        if constexpr (kA) {
+        if (kA && use_a) {
           int jt = 0;
           for (int q2 = 1; q2 < p.g.J; ++q2)
             if (mt * kUmmaBM >= p.g.col0[q2]) jt = q2;
@@ -270,6 +279,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       };
       for (int idx = 0; idx < P; ++idx) {
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, nt = tile / M_TILES;
+        ptx::mbar_arrive_expect_tx(&full[idx], S::kXBytes + a_bytes);
         ptx::tma_load_2d(sX + idx * S::kXBytes, &tmX, &full[idx], kb * kUmmaBK, nt * BN, pol_x);
         load_a(idx, tile % M_TILES, kb);
       }
@@ -279,7 +289,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks;
         const int mt = tile % M_TILES, nt = tile / M_TILES;
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+        ptx::mbar_arrive_expect_tx(&full[stage], S::kWBytes + S::kXBytes + a_bytes);
         ptx::tma_load_2d(sW + stage * S::kWBytes, &tmW, &full[stage], kb * kUmmaBK, mt * kUmmaBM, pol_w);
         ptx::tma_load_2d(sX + stage * S::kXBytes, &tmX, &full[stage], kb * kUmmaBK, nt * BN, pol_x);
         load_a(stage, mt, kb);
@@ -335,7 +345,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
 #pragma unroll
           for (int k = 0; k < kUmmaBK / 16; ++k)  // UMMA_K = 16 bf16 = 32 B -> +2 in the >>4 address field
             ptx::mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          if constexpr (kA) {  // K-local shrink: V[k][t] += A_a[k][kb] . X[t][kb] (rows >= 16 ignored)
+          if (kA && s_misc[8]) {  // K-local shrink: V[k][t] += A_a[k][kb] . X[t][kb] (rows >= 16 ignored)
             const uint64_t s_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * S::kABytes));
             const uint32_t v_tmem = tmem_base + (uint32_t)(2 * BN + acc * BN);
 #pragma unroll
@@ -441,6 +451,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     int cur_nt = -1;
     LoraPre pre;
     pre.a = -1;
+    pre.sb = S::kHasA ? s_preb + etid : nullptr;  // decode: B rows live in shared memory, not registers
     if (p.fuse && !local) {
       // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
       // Units (leader token t, slice j, rank row k) are computed by the epilogue warps while the
@@ -557,10 +568,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       ptx::named_bar_sync(1, 128);
       cur_nt = nt;
       if (!p.tcx) lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
-      if (local && pre.a >= 0) {  // park the gathered B rows in smem now: the loads complete during the stream
-#pragma unroll
-        for (int q2 = 0; q2 < 16; ++q2) s_preb[q2 * 128 + etid] = pre.b[q2];
-      }
+
     }
     if (p.fuse && !local) {
       // every unit of the launch published before any expand reads v
@@ -769,16 +777,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       pre_n = n;
       if (local) {
         // B rows of this thread's output column (the single adapter): gathered now, used after the stream
-        if (la >= 0 && pre.a != la) {
-          lora_pre16(pre, n, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
-          if (pre.a >= 0) {
-#pragma unroll
-            for (int q2 = 0; q2 < 16; ++q2) s_preb[q2 * 128 + etid] = pre.b[q2];
-          }
-        }
+        if (la >= 0 && pre.a != la) lora_pre16(pre, n, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
       } else if (!p.tcx) {
         lora_chunk16(lr, n, t0, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g, p.v, p.T, &pre, s_v, S::kVFloats,
-                     etid);
+                     etid, (p.trace && first_seg) ? p.trace + (size_t)blockIdx.x * 32 : nullptr);
       }
       if (first_seg && etid == 0) UMMA_TRACE(15);
       const bool was_first = first_seg;
@@ -1081,6 +1083,16 @@ inline bool cluster_splitk_enabled() {
   return g_cluster_mode == 1;
 }
 
+// K-local LoRA only for K segments of <= kLocalMaxKb k-blocks per CTA (BDLORA_LOCAL_MAXKB overrides)
+inline int local_max_kb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("BDLORA_LOCAL_MAXKB");
+    v = s ? std::max(0, atoi(s)) : 8;
+  }
+  return v;
+}
+
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
 
 // Workspace: [sync: 3 ints, 256 B][tile counters][split-tile partials]
@@ -1169,6 +1181,10 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
       }
     }
     if ((long long)mc * p1.cluster < p0.grid) p1.cluster = 1;
+    // the K-local LoRA adds a 2 KB A box to every k-block: worth it only where the tail dominates (cluster
+    // reduce, short K segments -- measured alone: 8B O (16 k-blocks/CTA) -1.5 us but +1 us in the layer chain, 8B down (56) +5 us); otherwise
+    // the grid-wide shrink hides under the stream
+    if (p1.cluster == 1 || p1.k_blocks / p1.cluster > local_max_kb()) p1.local = 0;
     if (getenv("BDLORA_DEBUG"))
       fprintf(stderr, "[bdlora] umma BN=%d grid=%d cluster=%d (max active clusters %d) -> %d\n", BN, p0.grid,
               p0.cluster, mc, p1.cluster);
@@ -1274,7 +1290,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   // K-local LoRA needs the arena's A-row tensor map and tiles that never straddle a slice boundary
   bool aligned = true;
   for (int j = 1; j < g.J; ++j) aligned = aligned && (g.col0[j] % kUmmaBM == 0);
-  p.local = (v_fused && amap && aligned && BN == 16) ? local_lora_mode() : 0;
+  p.local = (v_fused && amap && aligned && BN == 16 && p.cluster > 1) ? local_lora_mode() : 0;
   p.nstages = 0;  // set per BN
   p.route = nullptr;
   CUtensorMap tmW, tmX;

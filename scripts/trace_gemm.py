@@ -49,7 +49,7 @@ t = t[used]
 t0 = t[:, 0].min()
 names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit", "fin_beg",
          "fin_end", "arrived", "part_beg", "shr_done", "v_ready", "lora1",
-         "vseg_smem", "lr_done", "s18", "s19"]
+         "vseg_smem", "lr_done", "chunk_in", "v_staged", "lc_g", "lc_j", "lc_mask", "lc_vec"]
 print(f"M={M} K={K} T={T} event time {s.elapsed_time(e)*1e3:.1f} us, CTAs {used.sum()}")
 for k, nm in enumerate(names):
     if (t[:, k] <= 0).all():
