@@ -209,6 +209,55 @@ def row_partial_bd(X_full: np.ndarray, W: np.ndarray, adapter_inputs: Dict[int, 
     return P
 
 
+def row_partial_nfs(X_full: np.ndarray, W: np.ndarray, adapter_inputs: Dict[int, dict], ids: np.ndarray,
+                    n: int, i: int) -> np.ndarray:
+    """Per-device partial of an NFS-LoRA row layer ("adapters A_1 and B_2 are not sharded
+    across devices, but replicated so that each device maintains a full copy"; A_2 keeps the standard
+    row sharding of the base weight):
+
+        P_i = X^i W^i + s (X^i A_2[i*d_in/N:(i+1)*d_in/N, :]) B_2          (full rank r, full B_2)
+
+    The base all-reduce sums the partials (same collective count as BD-LoRA).  Sum over i is
+    pinned to `row_layer(..., "nfs", n)` (tests/test_oracle_pins.py)."""
+    X_full = np.asarray(X_full, dtype=np.float64)
+    d_in = X_full.shape[1]
+    bi = d_in // n
+    Xi = X_full[:, i * bi:(i + 1) * bi]
+    P = Xi @ np.asarray(W[i * bi:(i + 1) * bi, :], dtype=np.float64)
+    for a in sorted(set(int(v) for v in np.asarray(ids).tolist()) - {-1}):
+        ad = adapter_inputs[a]
+        A = np.asarray(ad["A"][0], dtype=np.float64)  # d_in x r, dense
+        B = np.asarray(ad["B"][0], dtype=np.float64)  # r x d_out, replicated
+        rows = np.nonzero(np.asarray(ids) == a)[0]
+        P[rows] += float(ad["scale"]) * (Xi[rows] @ A[i * bi:(i + 1) * bi, :] @ B)
+    return P
+
+
+def column_shard_nfs(X: np.ndarray, W: np.ndarray, d_out: Sequence[int], adapter_inputs: Dict[int, dict],
+                     ids: np.ndarray, n: int, i: int) -> np.ndarray:
+    """Device i of an NFS-LoRA column layer computed shard-locally: A_1 replicated (the full
+    v = X A_1, N-fold redundant), B_1 column-sharded like W_1:
+
+        Y^i_j = X W_j^(i) + s (X A_j) B_j[:, i*d_out_j/N:(i+1)*d_out_j/N]
+
+    Pinned to `column_layer(..., "nfs", n)` (tests/test_oracle_pins.py)."""
+    X = np.asarray(X, dtype=np.float64)
+    parts = []
+    c0 = 0
+    for j, dj in enumerate(d_out):
+        w = dj // n
+        Y = X @ np.asarray(W[:, c0 + i * w:c0 + (i + 1) * w], dtype=np.float64)
+        for a in sorted(set(int(v) for v in np.asarray(ids).tolist()) - {-1}):
+            ad = adapter_inputs[a]
+            A = np.asarray(ad["A"][j], dtype=np.float64)
+            B = np.asarray(ad["B"][j], dtype=np.float64)[:, i * w:(i + 1) * w]
+            rows = np.nonzero(np.asarray(ids) == a)[0]
+            Y[rows] += float(ad["scale"]) * ((X[rows] @ A) @ B)
+        parts.append(Y)
+        c0 += dj
+    return np.concatenate(parts, axis=1)
+
+
 def column_shard_bd(X: np.ndarray, W: np.ndarray, d_out: Sequence[int], adapter_inputs: Dict[int, dict],
                     ids: np.ndarray, n: int, i: int) -> np.ndarray:
     """Device i of a BD-LoRA column layer computed shard-locally, Alg. 2 lines 3-6:

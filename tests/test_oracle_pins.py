@@ -204,6 +204,76 @@ def test_column_layer_random_float_shard_equivalence():
         assert np.allclose(a, b, rtol=1e-12, atol=1e-12)
 
 
+# ----------------------------------------------------------------------------- NFS-LoRA
+
+def _bf_nfs_column_device(X, W, d_out, adapters, ids, n, i):
+    """Pure-Python NFS column device i: full A_1 (replicated), B_1 column block i."""
+    T, d_in = len(X), len(X[0])
+    cols, c0 = [], 0
+    for j, dj in enumerate(d_out):
+        w = dj // n
+        for cc in range(i * w, (i + 1) * w):
+            col = []
+            for t in range(T):
+                v = sum(X[t][d] * W[d][c0 + cc] for d in range(d_in))
+                a = ids[t]
+                if a >= 0:
+                    ad = adapters[a]
+                    for k in range(ad["rank"]):
+                        z = sum(X[t][d] * ad["A"][j][d][k] for d in range(d_in))
+                        v += ad["scale"] * z * ad["B"][j][k][cc]
+                col.append(v)
+            cols.append(col)
+        c0 += dj
+    return np.array(cols).T
+
+
+def _bf_nfs_row_partial(X, W, adapters, ids, n, i):
+    """Pure-Python NFS row partial on device i: A_2 row shard i (full rank), B_2 replicated."""
+    T, d_in, d_out = len(X), len(X[0]), len(W[0])
+    bi = d_in // n
+    P = [[0.0] * d_out for _ in range(T)]
+    for t in range(T):
+        for c in range(d_out):
+            v = sum(X[t][d] * W[d][c] for d in range(i * bi, (i + 1) * bi))
+            a = ids[t]
+            if a >= 0:
+                ad = adapters[a]
+                for k in range(ad["rank"]):
+                    z = sum(X[t][d] * ad["A"][0][d][k] for d in range(i * bi, (i + 1) * bi))
+                    v += ad["scale"] * z * ad["B"][0][k][c]
+            P[t][c] = v
+    return np.array(P)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_nfs_column_and_row_bruteforce(n):
+    """NFS-LoRA: replicated A_1 / B_2 make every device's LoRA term local (no LoRA
+    collective); the oracle's unsharded layer read off per device, its shard-local form, and the
+    pure-Python per-shard loops agree exactly on integers, and the row partials sum to the layer."""
+    rng = np.random.default_rng(40 + n)
+    d_in, d_out, r, T = 8, (8, 4), 3, 6   # NFS needs no N | r
+    ads = {a: {"rank": r, "scale": (2.0, -0.5)[a], "A": [_int_mat(rng, (d_in, r)) for _ in d_out],
+               "B": [_int_mat(rng, (r, dj)) for dj in d_out]} for a in range(2)}
+    X = _int_mat(rng, (T, d_in))
+    W = _int_mat(rng, (d_in, sum(d_out)))
+    ids = np.array([1, -1, 0, 0, 1, 1], dtype=np.int32)
+    full = ol.column_layer(X, W, d_out, ads, ids, "nfs", n)
+    for i in range(n):
+        ref = _bf_nfs_column_device(X.tolist(), W.tolist(), d_out, ads, ids.tolist(), n, i)
+        assert np.array_equal(ol.column_device_output(full, n, i), ref)
+        assert np.array_equal(ol.column_shard_nfs(X, W, d_out, ads, ids, n, i), ref)
+    rads = {a: {"rank": r, "scale": ad["scale"], "A": [ad["A"][0]], "B": [ad["B"][0][:, :6]]} for a, ad in ads.items()}
+    Wr = _int_mat(rng, (d_in, 6))
+    y = ol.row_layer(X, Wr, rads, ids, "nfs", n)
+    acc_ = np.zeros_like(y)
+    for i in range(n):
+        ref = _bf_nfs_row_partial(X.tolist(), Wr.tolist(), rads, ids.tolist(), n, i)
+        assert np.array_equal(ol.row_partial_nfs(X, Wr, rads, ids, n, i), ref)
+        acc_ += ref
+    assert np.array_equal(acc_, y)
+
+
 # ----------------------------------------------------------------------------- P3 / P4 / P5
 
 def test_n1_bd_is_plain_lora():
