@@ -70,11 +70,13 @@ typedef enum {
 } bdlora_status;
 
 enum { BDLORA_COLUMN = 0, BDLORA_ROW = 1 };
-enum { BDLORA_SHARD_BD = 0, BDLORA_SHARD_SLORA = 1 };
+/* BD-LoRA; S-LoRA; NFS-LoRA = A_1 and B_2 replicated, a full copy on every
+   device (same collectives as BD-LoRA, N x the memory and compute for A_1 and B_2).       */
+enum { BDLORA_SHARD_BD = 0, BDLORA_SHARD_SLORA = 1, BDLORA_SHARD_NFS = 2 };
 
 typedef struct {
   int32_t parallel;   /* BDLORA_COLUMN | BDLORA_ROW                                              */
-  int32_t sharding;   /* BDLORA_SHARD_BD | BDLORA_SHARD_SLORA                                    */
+  int32_t sharding;   /* BDLORA_SHARD_BD | BDLORA_SHARD_SLORA | BDLORA_SHARD_NFS                 */
   int32_t tp_size;    /* N >= 1                                                                  */
   int32_t tp_rank;    /* i in [0, N): block i lives on device i (reading R2)          */
   int32_t d_in;       /* FULL input dim                                                          */
@@ -82,7 +84,7 @@ typedef struct {
                          ROW requires 1.                                                         */
   int32_t d_out[BDLORA_MAX_SLICES]; /* FULL output dim per slice                                 */
   int32_t capacity;   /* resident adapter slots (ids index these)                                */
-  int32_t max_rank;   /* full-rank bound r_max; BD requires tp_size | every loaded rank          */
+  int32_t max_rank;   /* full-rank bound r_max; BD / S-LoRA column require tp_size | every rank  */
   int64_t arena_bytes;/* 0 = capacity x max_rank sizing; else a ragged first-fit arena of this size*/
 } bdlora_pool_desc;
 
@@ -105,8 +107,11 @@ int bdlora_set_pdl(int enable);
    partition of K (y = sum_seg X_seg W_seg + s (X_seg A_seg) B, regrouping matmul_3/4 and matmul_5/6 of
    Alg. 1/2), so each CTA streaming a K-range of W can add its own share of the LoRA term:
    0 = GLOBAL: v = s X A computed once by the grid, every CTA waits for the whole v before its expand;
-   1 = AUTO (default): K-local when the token tile's distinct adapters have sum(r/N) <= 64, else global;
-   2 = K-LOCAL whenever eligible (T <= 16, one v chunk).  Results agree to fp32 summation order.
+   1 = AUTO (default): K-local when the token tile holds ONE adapter group of rank <= 16 on this
+       device, the tiles are reduced through a thread-block cluster and every CTA's K segment is
+       short (<= 8 k-blocks, env BDLORA_LOCAL_MAXKB) -- the A rows then ride the weight pipeline as a
+       16-row TMA box per stage and a second tcgen05 MMA accumulates v_seg; else GLOBAL;
+   2 = same eligibility as 1 (kept for compatibility).  Results agree to fp32 summation order.
    Also settable with the environment variable BDLORA_LOCAL.  E_ARG for other values.                */
 int bdlora_set_decode_lora(int mode);
 /* Profiling hook: if non-NULL, subsequent tensor-core GEMM launches record per-CTA %globaltimer
@@ -138,6 +143,8 @@ int bdlora_destroy_pool(bdlora_pool* pool);
      ROW    + BD   : A[0] compact d_in x (r/N), the N diagonal blocks (d_in/N) x (r/N) stacked
                       ;  B[0] r x d_out
      *      + SLORA: dense A[j] d_in x r ;  B[j] r x d_out[j]
+     *      + NFS  : dense A[j] d_in x r ;  B[j] r x d_out[j]; the device keeps A_1 whole and B_1's
+                     column block i (COLUMN), A_2's row block i and B_2 whole (ROW)
    rank r: 1 <= r <= max_rank, BD needs N | r (else BDLORA_E_DIVISIBILITY).  scale = s_a applied to
    the fp32 shrink output (e.g. alpha*sqrt(N)/sqrt(r) for BD; reading R1).  src_is_device:
    0 = host pointers (copied synchronously w.r.t. `stream`; sources may be freed on return),
@@ -196,6 +203,20 @@ int slora_column_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, in
    -> base ncclAllReduce.  Pool ROW + SLORA.  +1 all-reduce.                                      */
 int slora_row_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
                       const int32_t* ids, void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+
+/* ---------------------------------------------------------------- NFS-LoRA comparison ------- */
+/* Column: every device holds the whole A_1, so v = s X A[a] (full rank, N-fold redundant)
+   is local, and B_1[:, cols i] expands into the device's columns -- no communication.  Same tensors
+   as bdlora_column_forward; pool COLUMN + NFS (no N | r requirement).                             */
+int nfs_column_forward(bdlora_pool* pool, const void* X, int64_t T, const void* W, const int32_t* ids,
+                       void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+/* Row: P_i = X_i W_i + s (X_i A[rows i, :]) B (B_2 whole on every device), then the base
+   model's all-reduce -- the only collective, as for BD-LoRA.  comm may be NULL iff
+   tp_size == 1; pool ROW + NFS.  nfs_row_partial is the same without the all-reduce.              */
+int nfs_row_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
+                    const int32_t* ids, void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+int nfs_row_partial(bdlora_pool* pool, const void* X, int64_t T, const void* W, const int32_t* ids,
+                    void* P, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
 
 /* ---------------------------------------------------------------- phases -------------------- */
 /* The two device-local halves of every path, for callers that run the collective themselves

@@ -18,10 +18,11 @@ from . import _lib
 from ._lib import BdloraError, PoolDesc, call
 
 COLUMN, ROW = 0, 1
-SHARD_BD, SHARD_SLORA = 0, 1
+SHARD_BD, SHARD_SLORA, SHARD_NFS = 0, 1, 2
 
 __all__ = [
-    "COLUMN", "ROW", "SHARD_BD", "SHARD_SLORA", "BdloraError", "Pool", "Comm",
+    "COLUMN", "ROW", "SHARD_BD", "SHARD_SLORA", "SHARD_NFS", "nfs_column_forward", "nfs_row_partial",
+    "nfs_row_forward", "BdloraError", "Pool", "Comm",
     "bdlora_abi_version", "bdlora_device_check", "bdlora_kernel_launches", "bdlora_comm_unique_id", "bdlora_comm_init",
     "bdlora_comm_destroy", "bdlora_comm_stats", "bdlora_create_pool", "bdlora_destroy_pool",
     "bdlora_load_adapter", "bdlora_unload_adapter", "bdlora_pool_bytes", "bdlora_pool_geometry",
@@ -312,6 +313,24 @@ def slora_column_forward(pool: Pool, comm: Optional[Comm], X, W, ids, Y, ws, str
 def slora_row_forward(pool: Pool, comm: Optional[Comm], X, W, ids, Y, ws, stream=None) -> None:
     T = _check_fwd(pool, X, W, ids, Y, ws, pool.k_loc, pool.m_loc)
     call("slora_row_forward", pool.handle, _comm_ptr(comm), _ptr(X), T, _ptr(W), _ptr(ids), _ptr(Y), _ptr(ws),
+         ws.numel(), _stream(stream))
+
+
+def nfs_column_forward(pool: Pool, X, W, ids, Y, ws, stream=None) -> None:
+    T = _check_fwd(pool, X, W, ids, Y, ws, pool.k_loc, pool.m_loc)
+    call("nfs_column_forward", pool.handle, _ptr(X), T, _ptr(W), _ptr(ids), _ptr(Y), _ptr(ws), ws.numel(),
+         _stream(stream))
+
+
+def nfs_row_partial(pool: Pool, X, W, ids, P, ws, stream=None) -> None:
+    T = _check_fwd(pool, X, W, ids, P, ws, pool.k_loc, pool.m_loc)
+    call("nfs_row_partial", pool.handle, _ptr(X), T, _ptr(W), _ptr(ids), _ptr(P), _ptr(ws), ws.numel(),
+         _stream(stream))
+
+
+def nfs_row_forward(pool: Pool, comm: Optional[Comm], X, W, ids, Y, ws, stream=None) -> None:
+    T = _check_fwd(pool, X, W, ids, Y, ws, pool.k_loc, pool.m_loc)
+    call("nfs_row_forward", pool.handle, _comm_ptr(comm), _ptr(X), T, _ptr(W), _ptr(ids), _ptr(Y), _ptr(ws),
          ws.numel(), _stream(stream))
 
 

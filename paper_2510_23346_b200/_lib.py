@@ -53,6 +53,9 @@ SIGNATURES = {
     "bdlora_row_forward": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "slora_column_forward": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "slora_row_forward": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "nfs_column_forward": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "nfs_row_partial": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "nfs_row_forward": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "bdlora_lora_shrink": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
     "bdlora_base_expand": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "bdlora_v_elems": (c_int, [c_vp, c_i64, ctypes.POINTER(c_i64)]),
@@ -66,7 +69,7 @@ def header_symbols(path: str | None = None):
     path = path or os.path.join(os.path.dirname(_PKG), "include", "bdlora.h")
     src = open(path).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+((?:bdlora|slora)_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+((?:bdlora|slora|nfs)_\w+)\s*\(", src, flags=re.M)))
 
 
 _lib = None

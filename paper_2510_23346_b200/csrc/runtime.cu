@@ -103,41 +103,33 @@ struct bdlora_pool {
 
 namespace {
 
-int64_t slot_elems_for_rank(const bdlora_pool* p, int r) {
-  const auto& d = p->d;
-  const int N = d.tp_size;
-  int rs, re;
-  if (d.sharding == BDLORA_SHARD_BD) {
-    rs = r / N;
-    re = r / N;
-  } else if (d.parallel == BDLORA_COLUMN) {
-    rs = r / N;
-    re = r;
-  } else {
-    rs = r;
-    re = r;
-  }
-  int64_t e = 0;
-  for (int j = 0; j < p->g.J; ++j) e += (int64_t)rs * p->g.K + (int64_t)re * p->ldb[j];
-  // slot regions are whole rows of K elements: every A row starts at a multiple of K, so one TMA
-  // tensor map over the arena ([arena_elems / K, K]) addresses any adapter's A rows (tensor-core shrink)
-  const int64_t K = p->g.K;
-  return (e + K - 1) / K * K;
-}
-
+// Rank rows of one slot on this device: rs rows of A (shrink), re rows of B (expand).
+//   BD: r/N and r/N;  S-LoRA column: r/N and r;  S-LoRA row: r and r;
+//   NFS: r and r -- A_1 / B_2 whole, A_2 / B_1 with the full rank.
 void ranks_for(const bdlora_pool* p, int r, int* rs, int* re) {
   const auto& d = p->d;
   const int N = d.tp_size;
   if (d.sharding == BDLORA_SHARD_BD) {
     *rs = r / N;
     *re = r / N;
-  } else if (d.parallel == BDLORA_COLUMN) {
+  } else if (d.sharding == BDLORA_SHARD_SLORA && d.parallel == BDLORA_COLUMN) {
     *rs = r / N;
     *re = r;
   } else {
     *rs = r;
     *re = r;
   }
+}
+
+int64_t slot_elems_for_rank(const bdlora_pool* p, int r) {
+  int rs, re;
+  ranks_for(p, r, &rs, &re);
+  int64_t e = 0;
+  for (int j = 0; j < p->g.J; ++j) e += (int64_t)rs * p->g.K + (int64_t)re * p->ldb[j];
+  // slot regions are whole rows of K elements: every A row starts at a multiple of K, so one TMA
+  // tensor map over the arena ([arena_elems / K, K]) addresses any adapter's A rows (tensor-core shrink)
+  const int64_t K = p->g.K;
+  return (e + K - 1) / K * K;
 }
 
 // Workspace layout (bytes, 256-aligned sections):
@@ -425,8 +417,9 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
   if (!desc || !out) return fail(BDLORA_E_ARG, "desc/out is NULL");
   const bdlora_pool_desc& d = *desc;
   if (d.parallel != BDLORA_COLUMN && d.parallel != BDLORA_ROW) return fail(BDLORA_E_ARG, "parallel = %d", d.parallel);
-  if (d.sharding != BDLORA_SHARD_BD && d.sharding != BDLORA_SHARD_SLORA)
+  if (d.sharding != BDLORA_SHARD_BD && d.sharding != BDLORA_SHARD_SLORA && d.sharding != BDLORA_SHARD_NFS)
     return fail(BDLORA_E_ARG, "sharding = %d", d.sharding);
+  const bool nfs = d.sharding == BDLORA_SHARD_NFS;
   if (d.tp_size < 1 || d.tp_rank < 0 || d.tp_rank >= d.tp_size)
     return fail(BDLORA_E_ARG, "tp_size = %d, tp_rank = %d", d.tp_size, d.tp_rank);
   if (d.n_slices < 1 || d.n_slices > BDLORA_MAX_SLICES) return fail(BDLORA_E_ARG, "n_slices = %d", d.n_slices);
@@ -438,7 +431,8 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
   if (d.max_rank < 1 || d.max_rank > 4096) return fail(BDLORA_E_CAPACITY, "max_rank = %d (1..4096)", d.max_rank);
   if (d.arena_bytes < 0) return fail(BDLORA_E_ARG, "arena_bytes < 0");
   const int N = d.tp_size;
-  if (d.max_rank % N) return fail(BDLORA_E_DIVISIBILITY, "max_rank %d not divisible by tp_size %d", d.max_rank, N);
+  if (!nfs && d.max_rank % N)
+    return fail(BDLORA_E_DIVISIBILITY, "max_rank %d not divisible by tp_size %d", d.max_rank, N);
   if (d.parallel == BDLORA_COLUMN) {
     for (int j = 0; j < d.n_slices; ++j)
       if (d.d_out[j] % N) return fail(BDLORA_E_DIVISIBILITY, "d_out[%d] = %d not divisible by tp_size %d", j, d.d_out[j], N);
@@ -472,10 +466,10 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
     }
     g.col0[g.J] = c0;
     g.M = c0;
-    g.Rc = d.max_rank / N;
+    g.Rc = nfs ? d.max_rank : d.max_rank / N;
     g.C = (d.sharding == BDLORA_SHARD_SLORA) ? N : 1;
-    p->rs_max = d.max_rank / N;
-    p->re_max = (d.sharding == BDLORA_SHARD_SLORA) ? d.max_rank : d.max_rank / N;
+    p->rs_max = nfs ? d.max_rank : d.max_rank / N;
+    p->re_max = (d.sharding == BDLORA_SHARD_BD) ? d.max_rank / N : d.max_rank;
   } else {
     g.K = d.d_in / N;
     g.J = 1;
@@ -488,6 +482,12 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
       p->ldb[0] = g.M;
       g.Rc = d.max_rank / N;
       p->rs_max = p->re_max = d.max_rank / N;
+    } else if (nfs) {  // B_2 whole on every device: expand window = all d_out columns
+      g.e_lo[0] = 0;
+      g.e_hi[0] = g.M;
+      p->ldb[0] = g.M;
+      g.Rc = d.max_rank;
+      p->rs_max = p->re_max = d.max_rank;
     } else {
       const int w = g.M / N;
       g.e_lo[0] = i * w;
@@ -594,7 +594,8 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
   const int N = d.tp_size, i = d.tp_rank, J = p->g.J;
   // BD: rank r/N per shard; S-LoRA column: rank chunks of r/N.  S-LoRA row keeps
   // the full rank on every device.
-  const bool need_div = !(d.sharding == BDLORA_SHARD_SLORA && d.parallel == BDLORA_ROW);
+  const bool need_div = !(d.sharding == BDLORA_SHARD_SLORA && d.parallel == BDLORA_ROW) &&
+                        d.sharding != BDLORA_SHARD_NFS;  // NFS replicates instead of splitting the rank
   if (need_div && rank % N)
     return fail(BDLORA_E_DIVISIBILITY, "rank %d not divisible by tp_size %d (P:462)", rank, N);
   if (!A || !B) return fail(BDLORA_E_ARG, "A/B arrays are NULL");
@@ -647,7 +648,14 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
     const int w = p->ldb[j];
     const uint16_t *sa = nullptr, *sb = nullptr;
     // ---- A_j -> [rs, K] ----
-    if (d.parallel == BDLORA_COLUMN) {
+    if (d.parallel == BDLORA_COLUMN && d.sharding == BDLORA_SHARD_NFS) {
+      // NFS: A_1 replicated -- the whole d_in x r on every device
+      rc = src_ptr(A[j], (int64_t)d.d_in * rank, &sa);
+      if (rc) break;
+      e.offA[j] = cur;
+      rc = gather_to(sa, rank, 0, 0, d.d_in, rank, 1, p->arena + cur, st);
+      cur += (int64_t)rs * K;
+    } else if (d.parallel == BDLORA_COLUMN) {
       // A_j full d_in x r; shard = columns [i*r/N, (i+1)*r/N) (BD and S-LoRA: column-sharded A_1)
       rc = src_ptr(A[j], (int64_t)d.d_in * rank, &sa);
       if (rc) break;
@@ -662,7 +670,7 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
       rc = gather_to(sa, rank / N, i * K, 0, K, rank / N, 1, p->arena + cur, st);
       cur += (int64_t)rs * K;
     } else {
-      // S-LoRA row: A_2 d_in x r row-sharded: rows [i*d_in/N, ...)
+      // S-LoRA / NFS row: A_2 d_in x r row-sharded: rows [i*d_in/N, ...)
       rc = src_ptr(A[0], (int64_t)d.d_in * rank, &sa);
       if (rc) break;
       e.offA[0] = cur;
@@ -678,11 +686,17 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
       e.offB[j] = curB;
       rc = gather_to(sb, dout, 0, i * w, rank / N, w, 0, p->arena + curB, st);
     } else if (d.parallel == BDLORA_COLUMN) {
-      // S-LoRA column: B_1 r x d_out_j column-sharded
+      // S-LoRA / NFS column: B_1 r x d_out_j column-sharded
       rc = src_ptr(B[j], (int64_t)rank * dout, &sb);
       if (rc) break;
       e.offB[j] = curB;
       rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + curB, st);
+    } else if (d.sharding == BDLORA_SHARD_NFS) {
+      // NFS row: B_2 replicated -- the whole r x d_out on every device
+      rc = src_ptr(B[0], (int64_t)rank * dout, &sb);
+      if (rc) break;
+      e.offB[0] = curB;
+      rc = gather_to(sb, dout, 0, 0, rank, dout, 0, p->arena + curB, st);
     } else if (d.sharding == BDLORA_SHARD_BD) {
       // BD row: B_2 r x d_out row-sharded: rows [i*r/N, ...)
       rc = src_ptr(B[0], (int64_t)rank * dout, &sb);
@@ -844,6 +858,46 @@ int bdlora_row_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t
   ST_TRY(bd_local(p, X, T, W, ids, Y, ws, st));
   if (p->d.tp_size > 1) {
     // Alg. 1 line 15: the base model's own all-reduce -- the only collective
+    const size_t n = (size_t)T * p->g.M;
+    NC_TRY(ncclAllReduce(Y, Y, n, ncclBfloat16, ncclSum, comm->nccl, st));
+    comm->counts[0] += 1;
+    comm->counts[3] += (int64_t)n * 2;
+  }
+  return BDLORA_OK;
+}
+
+// ---------------------------------------------------------------------------- NFS-LoRA
+// Replicated A_1 / B_2: every device's LoRA term is local, so the path is the BD one with
+// full-rank factors -- the same single-kernel decode forward, no LoRA collective.
+int nfs_column_forward(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y, void* ws,
+                       size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_COLUMN, BDLORA_SHARD_NFS, "nfs_column_forward"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  return bd_local(p, X, T, W, ids, Y, ws, (cudaStream_t)stream);
+}
+
+int nfs_row_partial(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* P, void* ws,
+                    size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, P, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_ROW, BDLORA_SHARD_NFS, "nfs_row_partial"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  return bd_local(p, X, T, W, ids, P, ws, (cudaStream_t)stream);
+}
+
+int nfs_row_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t T, const void* W, const int32_t* ids,
+                    void* Y, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_ROW, BDLORA_SHARD_NFS, "nfs_row_forward"));
+  ST_TRY(require_comm(p, comm, "nfs_row_forward"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  ST_TRY(bd_local(p, X, T, W, ids, Y, ws, st));
+  if (p->d.tp_size > 1) {
+    // the base model's own all-reduce -- the only collective
     const size_t n = (size_t)T * p->g.M;
     NC_TRY(ncclAllReduce(Y, Y, n, ncclBfloat16, ncclSum, comm->nccl, st));
     comm->counts[0] += 1;

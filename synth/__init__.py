@@ -192,7 +192,8 @@ class AdapterInput:
 
 def make_adapter(rng: np.random.Generator, proj: Projection, sharding: str, rank: int, n: int,
                  scale: float, zero: str = "") -> AdapterInput:
-    """One adapter's factors in load format for `sharding` in {"bd", "slora"}.
+    """One adapter's factors in load format for `sharding` in {"bd", "slora", "nfs"} (S-LoRA and NFS-LoRA
+    take dense factors, include/bdlora.h).
 
     zero: "" | "A" | "B"  -> force that factor to exact zeros (P5)."""
     J = len(proj.d_out)

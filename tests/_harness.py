@@ -86,7 +86,7 @@ def make_pool(case: Case, i: int, device: int = 0, arena_bytes: int = 0):
     import paper_2510_23346_b200 as bd
 
     par = bd.COLUMN if case.proj.parallel == "column" else bd.ROW
-    sh = bd.SHARD_BD if case.sharding == "bd" else bd.SHARD_SLORA
+    sh = {"bd": bd.SHARD_BD, "slora": bd.SHARD_SLORA, "nfs": bd.SHARD_NFS}[case.sharding]
     pool = bd.bdlora_create_pool(par, sh, case.n, i, case.proj.d_in, case.proj.d_out, case.capacity,
                                  case.max_rank, arena_bytes=arena_bytes, device=device)
     for a, ad in case.adapters.items():

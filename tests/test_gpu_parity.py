@@ -43,7 +43,7 @@ def run_column(case: H.Case, i: int, dev, fwd="bd"):
     T = X.shape[0]
     Y = torch.full((T, pool.m_loc), float("nan"), dtype=torch.bfloat16, device=dev)
     ws = bd.make_workspace(pool, T)
-    bd.bdlora_column_forward(pool, X, W, ids, Y, ws)
+    (bd.nfs_column_forward if case.sharding == "nfs" else bd.bdlora_column_forward)(pool, X, W, ids, Y, ws)
     torch.cuda.synchronize()
     pool.close()
     return Y
@@ -59,7 +59,7 @@ def run_row_partial(case: H.Case, i: int, dev):
     T = X.shape[0]
     P = torch.full((T, pool.m_loc), float("nan"), dtype=torch.bfloat16, device=dev)
     ws = bd.make_workspace(pool, T)
-    bd.bdlora_row_partial(pool, X, W, ids, P, ws)
+    (bd.nfs_row_partial if case.sharding == "nfs" else bd.bdlora_row_partial)(pool, X, W, ids, P, ws)
     torch.cuda.synchronize()
     pool.close()
     return P
@@ -245,6 +245,55 @@ def test_slora_row_8b_o(dev, n):
     _assert_tol(acc.cpu().numpy(), ol.row_layer(case.X.f64, case.W.f64, ads, case.ids, "slora", n), f"slora row N={n}")
     for p in pools:
         p.close()
+
+
+# ----------------------------------------------------------------------------- NFS-LoRA
+
+@pytest.mark.parametrize("n", [1, 2, 8])
+@pytest.mark.parametrize("T", [1, 5, 37])
+def test_nfs_column_8b_qkv(dev, n, T):
+    """NFS-LoRA column layer (A_1 replicated, B_1 column-sharded; no LoRA collective): every device's
+    block vs the oracle.  Ranks not divisible by N are legal for NFS (12 at N = 8)."""
+    proj = synth.arch_projections("llama-3.1-8b")[0]
+    case = H.make_case(1100 + 10 * n + T, proj, "nfs", n, T, ranks=[16, 12, 8])
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "nfs", n)
+    for i in sorted({0, n - 1}):
+        _assert_tol(_np(run_column(case, i, dev)), ol.column_device_output(ref_full, n, i), f"N={n} rank {i}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 8])
+@pytest.mark.parametrize("T", [1, 37])
+def test_nfs_row_8b_o(dev, n, T):
+    """NFS-LoRA row layer (A_2 row-sharded, B_2 replicated): per-rank partials vs the oracle's, and their
+    sum (the base all-reduce, emulated) vs the unsharded layer."""
+    proj = synth.arch_projections("llama-3.1-8b")[1]
+    case = H.make_case(1200 + 10 * n + T, proj, "nfs", n, T, ranks=[16, 24])
+    ads = case.oracle_adapters()
+    acc = None
+    for i in range(n):
+        P = _np(run_row_partial(case, i, dev))
+        _assert_tol(P, ol.row_partial_nfs(case.X.f64, case.W.f64, ads, case.ids, n, i), f"N={n} partial {i}")
+        acc = P if acc is None else acc + P
+    _assert_tol(acc, ol.row_layer(case.X.f64, case.W.f64, ads, case.ids, "nfs", n), f"N={n} sum")
+
+
+@pytest.mark.parametrize("n", [1, 4])
+@pytest.mark.parametrize("T", [9, 21])
+def test_nfs_integer_mode_bit_exact(dev, n, T):
+    """P10 for NFS-LoRA: column device blocks and row partials bit-identical to the oracle rounded once."""
+    col = synth.Projection("qkv", "column", 1024, (512, 256, 256))
+    case = H.make_case(1300 + n + T, col, "nfs", n, T, ranks=[8, 16, 8, 32], integer=True)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, col.d_out, case.oracle_adapters(), case.ids, "nfs", n)
+    for i in range(n):
+        got, ref = _np(run_column(case, i, dev)), ol.bf16_round(ol.column_device_output(ref_full, n, i))
+        assert np.array_equal(got, ref), f"column rank {i}: {np.count_nonzero(got != ref)} mismatches"
+    row = synth.Projection("down", "row", 1024, (512,))
+    case = H.make_case(1400 + n + T, row, "nfs", n, T, ranks=[8, 16, 32], integer=True)
+    ads = case.oracle_adapters()
+    for i in range(n):
+        got = _np(run_row_partial(case, i, dev))
+        ref = ol.bf16_round(ol.row_partial_nfs(case.X.f64, case.W.f64, ads, case.ids, n, i))
+        assert np.array_equal(got, ref), f"row rank {i}: {np.count_nonzero(got != ref)} mismatches"
 
 
 # ----------------------------------------------------------------------------- P10 integer mode
