@@ -152,7 +152,7 @@ class Projection:
                  w_replicas=None):
         self.proj, self.sharding, self.n, self.i = proj, sharding, n, i
         par = bd.COLUMN if proj.parallel == "column" else bd.ROW
-        sh = bd.SHARD_BD if sharding == "bd" else bd.SHARD_SLORA
+        sh = {"bd": bd.SHARD_BD, "slora": bd.SHARD_SLORA, "nfs": bd.SHARD_NFS}[sharding]
         cap = len(ranks_of_slots)
         self.pool = bd.bdlora_create_pool(par, sh, n, i, proj.d_in, proj.d_out, cap, max(ranks_of_slots), device=dev.index)
         k, m = self.pool.k_loc, self.pool.m_loc
@@ -188,6 +188,11 @@ class Projection:
                 bd.bdlora_column_forward(self.pool, X, W, ids, Y, self.ws)
             else:
                 bd.bdlora_row_forward(self.pool, comm, X, W, ids, Y, self.ws)
+        elif self.sharding == "nfs":
+            if self.proj.parallel == "column":
+                bd.nfs_column_forward(self.pool, X, W, ids, Y, self.ws)
+            else:
+                bd.nfs_row_forward(self.pool, comm, X, W, ids, Y, self.ws)
         else:
             if self.proj.parallel == "column":
                 bd.slora_column_forward(self.pool, comm, X, W, ids, Y, self.ws)
@@ -514,6 +519,18 @@ def run_ours(args, wl):
             p.close()
         del sl_layer
 
+    # ---------------- NFS-LoRA comparison (same box, same W) ----------------
+    nfs = None
+    if not args.skip_slora:
+        nf_layer, _ = build_layer(bd, torch, wl, "nfs", n, rank, dev, share_w=layer)
+        f_total, f_per, _ = time_layer(bd, torch, nf_layer, comm, ids, args.steps, args.warmup, not args.no_graph, barrier)
+        f_total = reduce_max(f_total, dev)
+        nfs = {"ms_per_step": f_total / args.steps, "tokens_per_s": T / (f_total / args.steps * 1e-3),
+               "proj_us": dict(zip(names, f_per)), "bd_speedup": (f_total / total_ms)}
+        for p in nf_layer:
+            p.close()
+        del nf_layer
+
     # ---------------- e2e through the public API with host buffers ----------------
     e2e_ms, h2d, d2h = time_e2e(bd, torch, layer, comm, ids_np, args.steps, args.warmup, barrier)
     e2e_ms = reduce_max(e2e_ms, dev)
@@ -531,7 +548,7 @@ def run_ours(args, wl):
         tp_emulated = {}
         for tpn in (2, 4, 8):
             row = {}
-            for sh in ("bd", "slora"):
+            for sh in ("bd", "slora", "nfs"):
                 em, _ = build_layer(bd, torch, wl, sh, tpn, 0, dev, seed=tpn)
                 # device-local work only (no collectives on one GPU): BD row = partial; S-LoRA = phases
                 tt, pp, _ = time_layer_local(bd, torch, em, ids, max(10, args.steps), args.warmup, tpn)
@@ -559,7 +576,7 @@ def run_ours(args, wl):
                        "cuda_graph": not args.no_graph, "parallelism": f"tp{n}"},
             "layer_us": ms_step * 1e3, "proj_us": proj_us, "layer_hbm_frac": layer_frac,
             "layer_algorithmic_bytes": layer_bytes,
-            "slora": slora, "collectives": collectives, "tp_emulated_1gpu": tp_emulated,
+            "slora": slora, "nfs": nfs, "collectives": collectives, "tp_emulated_1gpu": tp_emulated,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches * args.steps, "clocks": clk,
         }
@@ -574,8 +591,8 @@ def run_ours(args, wl):
 
 
 def time_layer_local(bd, torch, layer, ids, steps, warmup, tpn):
-    """Device-local per-rank work of one TP shard on one GPU (no collectives): BD column forward /
-    BD row partial / S-LoRA shrink + base_expand.  Graph-captured; returns (ms/step, proj us list)."""
+    """Device-local per-rank work of one TP shard on one GPU (no collectives): BD / NFS column forward,
+    BD / NFS row partial, S-LoRA shrink + base_expand.  Graph-captured; returns (ms/step, proj us list)."""
     dev = layer[0].X.device
     vbufs = {}
 
@@ -586,6 +603,11 @@ def time_layer_local(bd, torch, layer, ids, steps, warmup, tpn):
                 bd.bdlora_column_forward(p.pool, p.X, W, ids, p.Y, p.ws)
             else:
                 bd.bdlora_row_partial(p.pool, p.X, W, ids, p.Y, p.ws)
+        elif p.sharding == "nfs":
+            if p.proj.parallel == "column":
+                bd.nfs_column_forward(p.pool, p.X, W, ids, p.Y, p.ws)
+            else:
+                bd.nfs_row_partial(p.pool, p.X, W, ids, p.Y, p.ws)
         else:
             if id(p) not in vbufs:
                 T = p.X.shape[0]
@@ -613,7 +635,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="8b-decode-bs1-r16")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph")
-    ap.add_argument("--skip-slora", action="store_true")
+    ap.add_argument("--skip-slora", action="store_true", help="skip the S-LoRA and NFS-LoRA comparison legs")
     ap.add_argument("--skip-tp-emulation", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
