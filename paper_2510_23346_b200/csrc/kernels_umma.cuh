@@ -100,17 +100,21 @@ struct UmmaSmem {
   static constexpr int kVFloats = 4096;                              // 16 KB v staging (CUDA-core expand)
   // tensor-core expand operands (share the region with the v staging): A = B-slab^T [128 x Kp],
   // V_hi / V_lo = bf16 split of v [BN x Kp], K-major, no-swizzle core-matrix layout
-  static constexpr int kKp = BN <= 64 ? 64 : BN <= 128 ? 32 : 16;
+  static constexpr int kKp = BN <= 16 ? 64 : BN <= 128 ? 32 : 16;
+  static constexpr int kLoraBufs = (BN >= 32 && BN <= 128) ? 2 : 1;  // double-buffered operands
   static constexpr int kLoraA = 128 * kKp * 2;
   static constexpr int kLoraV = BN * kKp * 2;
   static constexpr int kLoraBytes = kLoraA + 2 * kLoraV;
-  static constexpr int kRegion = kLoraBytes > kVFloats * 4 ? kLoraBytes : kVFloats * 4;
+  static constexpr int kRegion = kLoraBufs * kLoraBytes > kVFloats * 4 ? kLoraBufs * kLoraBytes : kVFloats * 4;
   static constexpr int kMetaOff = kVOff + kRegion;                  // [BN][8] ints: leader re / offB (tc expand)
   // cluster split-K (decode): [s][ceil(128/s)][BN] fp32 partial slots pushed by the peers (dedicated: a peer
   // may push while this CTA still streams)
   static constexpr int kPartOff = kMetaOff + BN * 8 * 4;
   static constexpr int kPartBytes = kHasA ? (kUmmaBM + 8) * BN * 4 : 0;
-  static constexpr int kPreBOff = kPartOff + kPartBytes;              // [16][128] fp32 pre-gathered B rows
+  // tensor-core expand: the token tile's v rows staged once per segment (when they fit)
+  static constexpr int kVStOff = kPartOff + kPartBytes;
+  static constexpr int kVStBytes = BN == 64 ? 16384 : BN == 32 ? 12288 : 0;
+  static constexpr int kPreBOff = kVStOff + kVStBytes;               // [16][128] fp32 pre-gathered B rows
   static constexpr int kPreBBytes = kHasA ? 16 * 128 * 4 : 0;
   static constexpr int kBytes = kPreBOff + kPreBBytes + 1024;        // + alignment slack
   // the shrink MMA reads 128 rows (16 KB) from a stage's A box: rows 16..127 must stay inside the allocation
@@ -134,9 +138,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* lora_full = tempty + 2;   // tensor-core expand: operands built (128 epilogue arrivals)
-  uint64_t* lora_empty = lora_full + 1;  // tensor-core expand: operand MMAs done (tcgen05.commit)
-  uint32_t* tmem_holder = (uint32_t*)(lora_empty + 1);
+  uint64_t* lora_full = tempty + 2;   // [2] tensor-core expand: operands built (128 epilogue arrivals)
+  uint64_t* lora_empty = lora_full + 2;  // [2] tensor-core expand: operand MMAs done (tcgen05.commit)
+  uint32_t* tmem_holder = (uint32_t*)(lora_empty + 2);
   int* s_last = (int*)(tmem_holder + 1);
   int* s_ids = (int*)(smem + S::kBarOff + 256);  // [BN] adapter ids of the current token tile
   int* s_lead = s_ids + 256;                     // [BN] group leader of each token in its 16-chunk
@@ -144,12 +148,13 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   int* s_mem = s_fids + 256;                     // [T] members of the current adapter group
   int* s_isl = s_mem + 256;                      // [T] 1 if the token is the first of its adapter id
   float* s_red = (float*)(s_isl + 256);          // [4][4] cross-warp partial dots
-  int* s_misc = (int*)(s_red + 16);              // [0] claimed unit, [1] member count, [2] pass K, [3] last
-  int* s_pcol = s_misc + 16;                     // [8][6] tensor-core expand pass columns (a, j, k0, re, boff lo/hi)
+  int* s_misc = (int*)(s_red + 16);              // [0] claim [1] members [2..5] pass K/last per buffer [6] columns [8] K-local [12..15] scan
+  int* s_pcol = s_misc + 16;                     // [2][8][6] tensor-core expand pass columns (a, j, k0, re, boff)
   int* s_gmeta = (int*)(smem + S::kMetaOff);     // [BN][8] per leader token: re, offB[0..2] (lo, hi)
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
   float* s_preb = (float*)(smem + S::kPreBOff);  // decode: [16][128] B rows of each thread's column (parked)
   float* s_part = (float*)(smem + S::kPartOff);  // cluster split-K partial slots
+  float* s_vst = (float*)(smem + S::kVStOff);    // tensor-core expand: [C][tv][J][Rc] v of the token tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
@@ -182,8 +187,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
-    ptx::mbar_init(lora_full, 128);
-    ptx::mbar_init(lora_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(lora_full + b, 128);
+      ptx::mbar_init(lora_empty + b, 1);
+    }
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
@@ -308,7 +315,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      uint32_t lf_phase = 0;
+      int lbuf = 0;                    // tensor-core expand: next operand buffer
+      uint32_t lf_phase[2] = {0u, 0u};  // its mbarrier parity
       for (int u = u_lo; u < u_hi;) {
         const int tile = u / p.k_blocks;
         const int kb0 = u - tile * p.k_blocks;
@@ -316,24 +324,26 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        // LoRA expand passes (tensor-core expand duty = this CTA finishes the tile's k range): issued as soon
-        // as the epilogue warps have built them, interleaved with the base k-blocks (accumulation order is
-        // free in fp32), so the operand gathers overlap the weight stream instead of trailing it
-        const bool lduty = (MODE == 0) && p.tcx && kb1 == p.k_blocks;
+        // LoRA expand passes (every contributor of the tile takes its share, possibly one empty "last" pass):
+        // issued as soon as the epilogue warps have built them, interleaved with the base k-blocks
+        // (accumulation order is free in fp32), so the operand gathers overlap the weight stream
+        const bool lduty = (MODE == 0) && p.tcx;
         bool ldone = !lduty;
-        const uint32_t la0 = ptx::smem_u32(smem + S::kVOff);
         auto lora_pass = [&]() {
           constexpr uint32_t kSbo = (S::kKp / 8) * 128;  // V: 8-row group stride
+          const int b = lbuf;
+          const uint32_t la0 = ptx::smem_u32(smem + S::kVOff + b * S::kLoraBytes);
           const uint32_t vh0 = la0 + S::kLoraA, vl0 = vh0 + S::kLoraV;
-          lf_phase ^= 1u;
+          lf_phase[b] ^= 1u;
+          lbuf = (lbuf + 1) % S::kLoraBufs;
           ptx::tc_fence_after();
-          const int kp = s_misc[2], last = s_misc[3];
+          const int kp = s_misc[2 + 2 * b], last = s_misc[3 + 2 * b];
           for (int kk = 0; kk < kp / 16; ++kk) {  // A is MN-major (idesc_lora), V K-major
             const uint64_t ad = ptx::sdesc_k_none(la0 + kk * 4096, /*LBO: k-group*/ 2048, /*SBO: n-group*/ 128);
             ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vh0 + kk * 256, 128, kSbo), idesc_lora, 1u);
             ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vl0 + kk * 256, 128, kSbo), idesc_lora, 1u);
           }
-          ptx::mma_commit(lora_empty);
+          ptx::mma_commit(lora_empty + b);
           if (last) ldone = true;
         };
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -357,30 +367,11 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             stage = 0;
             phase ^= 1;
           }
-          if (!ldone && ptx::mbar_test(lora_full, lf_phase)) lora_pass();  // D already initialised (kb0 done)
+          if (!ldone && ptx::mbar_test(lora_full + lbuf, lf_phase[lbuf])) lora_pass();  // D initialised (kb0 done)
         }
         while (!ldone) {
-          ptx::mbar_wait(lora_full, lf_phase);
+          ptx::mbar_wait(lora_full + lbuf, lf_phase[lbuf]);
           lora_pass();
-        }
-        if (false) {
-          // LoRA expand passes: D += A_lora . V_hi^T + A_lora . V_lo^T over the packed K of this pass
-          const uint32_t a0 = ptx::smem_u32(smem + S::kVOff);
-          const uint32_t vh0 = a0 + S::kLoraA, vl0 = vh0 + S::kLoraV;
-          constexpr uint32_t kSbo = (S::kKp / 8) * 128;  // 8-row group stride
-          for (;;) {
-            ptx::mbar_wait(lora_full, lf_phase);
-            lf_phase ^= 1u;
-            ptx::tc_fence_after();
-            const int kp = s_misc[2], last = s_misc[3];
-            for (int kk = 0; kk < kp / 16; ++kk) {  // A is MN-major (idesc_ab), V K-major
-              const uint64_t ad = ptx::sdesc_k_none(a0 + kk * 4096, /*LBO: k-group*/ 2048, /*SBO: n-group*/ 128);
-              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vh0 + kk * 256, 128, kSbo), idesc_lora, 1u);
-              ptx::mma_bf16(d_tmem, ad, ptx::sdesc_k_none(vl0 + kk * 256, 128, kSbo), idesc_lora, 1u);
-            }
-            ptx::mma_commit(lora_empty);
-            if (last) break;
-          }
         }
         ptx::mma_commit(&tfull[acc]);
         UMMA_TRACE(4);
@@ -413,18 +404,19 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       ptx::named_bar_sync(1, 128);
       const int mt_a = (u_lo / p.k_blocks) % M_TILES;
       const int mt_b = ((u_hi - 1) / p.k_blocks) % M_TILES;
-      for (int t = 0; t < p.T; ++t) {  // uniform loop over distinct adapters (leaders)
+      // one thread per distinct adapter: its slot entry is read once (all threads' reads in flight together,
+      // not one dependent round trip per adapter), then the prefetches are fire-and-forget
+      for (int t = etid; t < p.T; t += 128) {
         if (!s_isl[t]) continue;
-        const int a = s_fids[t];
-        const SlotEntry* e = p.tab + a;
+        const SlotEntry e = p.tab[s_fids[t]];
         for (int mt = mt_a; mt <= mt_b; ++mt) {  // B rows of my output columns
           const int n0 = mt * kUmmaBM;
           for (int jj = 0; jj < p.g.J; ++jj) {
             const int lo = max(n0, p.g.e_lo[jj]), hi = min(n0 + kUmmaBM, p.g.e_hi[jj]);
             if (lo >= hi) continue;
             const int ldb = p.g.e_hi[jj] - p.g.e_lo[jj];
-            for (int k = etid; k < e->re; k += 128)
-              ptx::prefetch_l2_bulk(p.arena + e->offB[jj] + (size_t)k * ldb + (lo - p.g.e_lo[jj]), (hi - lo) * 2);
+            for (int k = 0; k < e.re; ++k)
+              ptx::prefetch_l2_bulk(p.arena + e.offB[jj] + (size_t)k * ldb + (lo - p.g.e_lo[jj]), (hi - lo) * 2);
           }
         }
       }
@@ -583,7 +575,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     uint32_t acc_phase = 0;
     bool first_seg = true;
     int pre_n = -1;
-    uint32_t le_phase = 0;
+    int lp = 0;  // tensor-core expand passes built so far (buffer = lp % kLoraBufs)
     for (int u = u_lo; u < u_hi;) {
       const int tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks;
@@ -630,83 +622,117 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::named_bar_sync(1, 128);
         cur_nt = nt;
       }
-      if (p.tcx && kb1 == p.k_blocks) {
-        // ---- tensor-core expand operands of this tile, built while its weights stream -------------------
-        // rank columns of the tile's (adapter group, slice) pairs packed in passes of kKp; per pass:
-        // A[n][k] = B_{a,j}[k][n] (rows n of slice j inside its expand window, else 0) and
-        // V[t][k] = v[t][j][k] split into bf16 hi + lo (tokens of group a, else 0); the MMA warp adds
-        // A.V_hi^T + A.V_lo^T into this tile's TMEM accumulator (fp32) -- one rounding at the store.
+      if (p.tcx) {
+        // ---- tensor-core expand: this CTA's share of the tile's LoRA columns, built while weights stream ----
+        // The tile's rank columns (leader i, slice j in [jlo, jhi], 8-row block) are numbered in (i, j, block)
+        // order through a parallel prefix over the tile's adapter groups; passes of KC columns are dealt
+        // round-robin to the tile's split contributors (the LoRA term is linear: every contributor adds its
+        // share into its own accumulator/partial).  Per pass: A[n][k] = B_{a,j}[k][n] (cp.async gathers of
+        // 16 contiguous bytes of a B row) and V[t][k] = v[t][j][k] split into bf16 hi + lo; the MMA warp adds
+        // A.V_hi^T + A.V_lo^T into the TMEM accumulator.  Operands are double-buffered: pass p+1 is gathered
+        // while the tensor cores consume pass p.
         const int n0 = mt * kUmmaBM;
         int jlo = 0, jhi = 0;
         for (int q2 = 1; q2 < p.g.J; ++q2) {
           if (n0 >= p.g.col0[q2]) jlo = q2;
           if (min(n0 + kUmmaBM - 1, p.g.M - 1) >= p.g.col0[q2]) jhi = q2;
         }
-        int jn = 0;
-        for (int q2 = 1; q2 < p.g.J; ++q2)
-          if (n >= p.g.col0[q2]) jn = q2;
-        const bool in_win = n < p.g.M && n >= p.g.e_lo[jn] && n < p.g.e_hi[jn];
-        uint8_t* la = smem + S::kVOff;
-        uint8_t* lvh = la + S::kLoraA;
-        uint8_t* lvl = lvh + S::kLoraV;
-        constexpr int KC = S::kKp / 8;  // core-matrix columns per pass
-        int ci = 0, cj = jlo, ccol = 0;  // pass cursor (thread 0)
-        bool done = false;
-        while (!done) {
-          if (etid == 0) {  // next pass: up to KC columns of 8 rank rows, metadata for all threads
-            int ncol = 0;
-            while (ncol < KC) {
-              if (ci >= tv) break;
-              if (!s_mem[ci]) {
-                ++ci;
-                cj = jlo;
-                ccol = 0;
-                continue;
-              }
-              const int a = s_ids[ci];
-              const int* gm = s_gmeta + ci * 8;
-              const int re = gm[0];
-              if (ccol >= (re + 7) / 8) {
-                ccol = 0;
-                if (++cj > jhi) {
-                  cj = jlo;
-                  ++ci;
-                }
-                continue;
-              }
-              int* pc = s_pcol + ncol * 6;
-              pc[0] = a, pc[1] = cj, pc[2] = ccol * 8, pc[3] = re, pc[4] = gm[1 + 2 * cj], pc[5] = gm[2 + 2 * cj];
-              ++ncol;
-              ++ccol;
-            }
-            // look ahead: is anything left after this pass?
-            while (ci < tv && !s_mem[ci]) ++ci;
-            s_misc[4] = ncol;
-            s_misc[5] = (ci >= tv) ? 1 : 0;
+        constexpr int KC = S::kKp / 8;  // core-matrix columns (8 rank rows each) per pass
+        // exclusive prefix of column counts over the tile's tokens -> s_gmeta[i * 8 + 7]; total in s_misc[6]
+        {
+          const int nsl = jhi - jlo + 1;
+          int c0v = 0, c1v = 0;
+          const int i0 = 2 * etid, i1 = 2 * etid + 1;
+          if (i0 < tv && s_mem[i0]) c0v = nsl * ((s_gmeta[i0 * 8] + 7) / 8);
+          if (i1 < tv && s_mem[i1]) c1v = nsl * ((s_gmeta[i1 * 8] + 7) / 8);
+          int incl = c0v + c1v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          const int we = etid >> 5;
+          if (lane == 31) s_misc[12 + we] = incl;
+          ptx::named_bar_sync(1, 128);
+          int woff = 0;
+          for (int w2 = 0; w2 < we; ++w2) woff += s_misc[12 + w2];
+          const int ex = woff + incl - (c0v + c1v);
+          if (i0 < tv) s_gmeta[i0 * 8 + 7] = ex;
+          if (i1 < tv) s_gmeta[i1 * 8 + 7] = ex + c0v;
+          if (etid == 127) s_misc[6] = woff + incl;
+          ptx::named_bar_sync(1, 128);
+        }
+        const int c_tot = s_misc[6];
+        // v rows of this token tile -> shared memory in one round trip (the passes then build V from smem)
+        const int per_c = tv * p.g.J * p.g.Rc;
+        const bool vst = c_tot > 0 && per_c * p.g.C * 4 <= S::kVStBytes;
+        if (vst) {
+          for (int idx = etid; idx < per_c * p.g.C; idx += 128) {
+            const int ch = idx / per_c, r2 = idx - ch * per_c;
+            s_vst[idx] = __ldg(p.v + (size_t)(ch * p.T + t0) * p.g.J * p.g.Rc + r2);
           }
           ptx::named_bar_sync(1, 128);
-          const int ncol = s_misc[4];
-          done = s_misc[5] != 0;
-          ptx::mbar_wait(lora_empty, le_phase ^ 1u);  // previous pass's MMAs have read the operands
+        }
+        const float* vb = vst ? s_vst : p.v + (size_t)t0 * p.g.J * p.g.Rc;  // token t of the tile at vb[t*J*Rc]
+        const int vT = vst ? tv : p.T;                                      // chunk stride in tokens
+        if (etid == 0 && lp == 0) UMMA_TRACE(19);
+        const int npass = (c_tot + KC - 1) / KC;
+        const int ts = tile * p.k_blocks;
+        const int c_first = umma_cta_of(ts, UNITS, GRID);
+        const int cs = umma_cta_of(ts + p.k_blocks - 1, UNITS, GRID) - c_first + 1, ci = cta - c_first;
+        const int my_n = max(1, npass > ci ? (npass - ci + cs - 1) / cs : 0);  // >= 1: an empty "last" pass
+        for (int m = 0; m < my_n; ++m) {
+          const int pp = ci + m * cs;
+          const int b = lp % S::kLoraBufs;
+          const uint32_t par = (uint32_t)(lp / S::kLoraBufs) & 1u;
+          int* pcb = s_pcol + b * 48;
+          uint8_t* la = smem + S::kVOff + b * S::kLoraBytes;
+          uint8_t* lvh = la + S::kLoraA;
+          uint8_t* lvl = lvh + S::kLoraV;
+          if (etid < KC) {  // column metadata: owning leader by binary search over the prefix
+            const int q = pp * KC + etid;
+            int* pc = pcb + etid * 6;
+            if (q < c_tot) {
+              int lo = 0, hi = tv - 1;
+              while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_gmeta[mid * 8 + 7] <= q) lo = mid;
+                else hi = mid - 1;
+              }
+              const int* gm = s_gmeta + lo * 8;
+              const int re = gm[0], nb = (re + 7) / 8, rem = q - gm[7];
+              const int cj = jlo + rem / nb;
+              pc[0] = s_ids[lo], pc[1] = cj, pc[2] = (rem % nb) * 8, pc[3] = re, pc[4] = gm[1 + 2 * cj],
+              pc[5] = gm[2 + 2 * cj];
+            } else {
+              pc[0] = -2, pc[1] = 0, pc[2] = 0, pc[3] = 0, pc[4] = 0, pc[5] = 0;
+            }
+          }
+          ptx::named_bar_sync(1, 128);
+          if (etid == 0 && lp < 2) UMMA_TRACE(20 + 4 * lp);
+          ptx::mbar_wait(lora_empty + b, par ^ 1u);  // the MMAs of this buffer's previous pass are done
+          if (etid == 0 && lp < 2) UMMA_TRACE(21 + 4 * lp);
           // A = B-slab^T in the MN-major no-swizzle layout: a 16-byte chunk is 8 consecutive output columns
-          // of one rank row k -- exactly 16 contiguous bytes of B's row k, so the gather is a plain
-          // coalesced LDG.128 -> STS.128 (core matrix (n-group, k-group) at (kg * 16 + ng) * 128, row k % 8)
+          // of one rank row k -- exactly 16 contiguous bytes of B's row k (core matrix (n-group, k-group)
+          // at (kg * 16 + ng) * 128, row k % 8)
 #pragma unroll
           for (int it = 0; it < S::kKp * 16 / 128; ++it) {
             const int idx = etid + it * 128;
             const int kr = idx >> 4, ng = idx & 15, c = kr >> 3;
-            const int* pc = s_pcol + c * 6;
-            uint4 val = make_uint4(0u, 0u, 0u, 0u);
+            const int* pc = pcb + c * 6;
+            uint8_t* dst = la + ((kr >> 3) * 16 + ng) * 128 + (kr & 7) * 16;
             const int k = pc[2] + (kr & 7);
-            if (c < ncol && k < pc[3]) {
+            bool zero = true;
+            if (k < pc[3]) {
               const int cjj = pc[1];
               const int lo = p.g.e_lo[cjj], hi = min(p.g.e_hi[cjj], p.g.M), ldb = p.g.e_hi[cjj] - lo;
               const int nlo = n0 + ng * 8;
               const long long boff = (long long)(unsigned)pc[4] | ((long long)pc[5] << 32);
               const uint16_t* Brow = reinterpret_cast<const uint16_t*>(p.arena + boff) + (size_t)k * ldb;
               if (nlo >= lo && nlo + 8 <= hi && (((uintptr_t)(Brow + (nlo - lo))) & 15) == 0) {
-                val = __ldg(reinterpret_cast<const uint4*>(Brow + (nlo - lo)));
-              } else {
+                ptx::cp_async_16(dst, Brow + (nlo - lo));
+                zero = false;
+              } else if (nlo + 8 > lo && nlo < hi) {
                 uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
                 for (int e2 = 0; e2 < 8; ++e2) {
@@ -714,25 +740,27 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                   const uint32_t h = (nn >= lo && nn < hi) ? (uint32_t)__ldg(Brow + (nn - lo)) : 0u;
                   w[e2 >> 1] |= h << ((e2 & 1) * 16);
                 }
-                val = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                zero = false;
               }
             }
-            *reinterpret_cast<uint4*>(la + ((kr >> 3) * 16 + ng) * 128 + (kr & 7) * 16) = val;
+            if (zero) *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
           }
+          if (etid == 0 && lp == 0) UMMA_TRACE(28);
           // V_hi / V_lo: (token, column) pairs over the 128 threads
 #pragma unroll
           for (int it = 0; it < (BN * KC + 127) / 128; ++it) {
             const int idx = etid + it * 128;
             if (idx >= BN * KC) break;
             const int t = idx / KC, c = idx - t * KC;
-            const int* pc = s_pcol + c * 6;
+            const int* pc = pcb + c * 6;
             float f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            if (c < ncol && t < tv && s_ids[t] == pc[0]) {
+            if (t < tv && s_ids[t] == pc[0]) {
               const int cjj = pc[1], ck = pc[2], re = pc[3], rcc = re / p.g.C;
-              const float* vrow = p.v + ((size_t)(t0 + t) * p.g.J + cjj) * p.g.Rc + ck;
+              const float* vrow = vb + ((size_t)t * p.g.J + cjj) * p.g.Rc + ck;
               if (p.g.C == 1 && ck + 8 <= re && (p.g.Rc & 3) == 0) {
-                const float4 f0 = __ldg(reinterpret_cast<const float4*>(vrow));
-                const float4 f1 = __ldg(reinterpret_cast<const float4*>(vrow + 4));
+                const float4 f0 = *reinterpret_cast<const float4*>(vrow);
+                const float4 f1 = *reinterpret_cast<const float4*>(vrow + 4);
                 f[0] = f0.x, f[1] = f0.y, f[2] = f0.z, f[3] = f0.w, f[4] = f1.x, f[5] = f1.y, f[6] = f1.z, f[7] = f1.w;
               } else {
 #pragma unroll
@@ -740,7 +768,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
                   const int k = ck + q2;
                   if (k < re) {
                     const int ch = k / rcc, kk = k - ch * rcc;
-                    f[q2] = __ldg(p.v + ((size_t)(ch * p.T + t0 + t) * p.g.J + cjj) * p.g.Rc + kk);
+                    f[q2] = vb[((size_t)(ch * vT + t) * p.g.J + cjj) * p.g.Rc + kk];
                   }
                 }
               }
@@ -758,14 +786,17 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             *reinterpret_cast<uint4*>(lvh + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
             *reinterpret_cast<uint4*>(lvl + off) = make_uint4(l4[0], l4[1], l4[2], l4[3]);
           }
+          if (etid == 0 && lp < 2) UMMA_TRACE(22 + 4 * lp);
+          ptx::cp_async_wait_all();
           ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
+          if (etid == 0 && lp < 2) UMMA_TRACE(23 + 4 * lp);
           if (etid == 0) {
-            s_misc[2] = ((ncol * 8 + 15) / 16) * 16;
-            s_misc[3] = done ? 1 : 0;
+            const int nvalid = max(0, min(KC, c_tot - pp * KC));
+            s_misc[2 + 2 * b] = ((nvalid * 8 + 15) / 16) * 16;
+            s_misc[3 + 2 * b] = (m == my_n - 1) ? 1 : 0;
           }
-          ptx::mbar_arrive(lora_full);
-          ptx::named_bar_sync(1, 128);  // s_pcol / s_misc reused by the next pass
-          le_phase ^= 1u;
+          ptx::mbar_arrive(lora_full + b);
+          ++lp;
         }
       }
       // LoRA term of the first 16 tokens on CUDA cores (when not on the tensor cores), gathered BEFORE

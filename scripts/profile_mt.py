@@ -51,15 +51,40 @@ e.record()
 torch.cuda.synchronize()
 print(f"{proj.name} TP{n} T={T}: {s.elapsed_time(e) / 10 * 1e3:.1f} us/call (eager)")
 if trace:
-    tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
+    tr = torch.zeros(148 * 32, dtype=torch.int64, device=dev)
     bd.bdlora_debug_trace(tr)
     fwd()
     torch.cuda.synchronize()
     bd.bdlora_debug_trace(None)
-    t = tr.view(148, 16).cpu().numpy().astype("int64")
+    t = tr.view(148, 32).cpu().numpy().astype("int64")
     t = t[t[:, 0] > 0]
     t0 = t[:, 0].min()
-    names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit"]
+    names = ["entry", "setup", "tma0", "data0", "mma_last", "epi_first", "epi_last", "epi_end", "exit"] + [""] * 10 + \
+        ["lx_pre", "p0_meta", "p0_empty", "p0_issued", "p0_landed", "p1_meta", "p1_empty", "p1_issued", "p1_landed",
+         "p0_a_issued"]
     for kk, nm in enumerate(names):
-        col = (t[:, kk] - t0) / 1e3
+        if not nm or (t[:, kk] <= 0).all():
+            continue
+        col = (t[:, kk][t[:, kk] > 0] - t0) / 1e3
         print(f"{nm:10s} min {col.min():8.2f} med {np.median(col):8.2f} max {col.max():8.2f}")
+
+if len(sys.argv) > 4 and sys.argv[4] == "parts":
+    # component timing: shrink alone, GEMM + expand alone, GEMM without LoRA
+    v = torch.zeros(bd.bdlora_v_elems(pool, T), dtype=torch.float32, device=dev)
+    nids = -torch.ones(T, dtype=torch.int32, device=dev)
+
+    def timeit(fn, reps=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps * 1e3
+
+    print(f"  shrink (route + tc shrink): {timeit(lambda: bd.bdlora_lora_shrink(pool, X, ids, v, ws)):.1f} us")
+    print(f"  base_expand (GEMM + expand): {timeit(lambda: bd.bdlora_base_expand(pool, X, W, ids, v, Y, ws)):.1f} us")
+    print(f"  base_expand, ids = -1:      {timeit(lambda: bd.bdlora_base_expand(pool, X, W, nids, v, Y, ws)):.1f} us")
+    print(f"  forward, ids = -1:          {timeit(lambda: fwd_nolora()) if False else 0:.1f}")
