@@ -560,6 +560,19 @@ def run_ours(args, wl):
                 torch.cuda.empty_cache()
             tp_emulated[f"tp{tpn}"] = row
 
+    # ---------------- whole decode step, batch-1 workloads ----------------
+    decode_step = None
+    if T == 1 and args.decode_layers > 0:
+        L = args.decode_layers
+        us = time_decode_step(bd, torch, wl, n, rank, dev, comm, max(3, args.steps // 10), args.warmup, L)
+        decode_step = {"layers": L, "us_per_token": us, "tokens_per_s": 1e6 / us,
+                       "note": "QKV->O->gate_up->down per layer chained through real inputs (attention / SiLU "
+                               "placeholders), one CUDA graph, PDL; per output token at batch 1"}
+        if world == 1 and not args.skip_tp_emulation:
+            decode_step["tp_emulated_1gpu"] = {
+                f"tp{tpn}": time_decode_step(bd, torch, wl, tpn, 0, dev, None, max(3, args.steps // 10), args.warmup,
+                                             L, local_only=True) for tpn in (2, 4, 8)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline(wl)
@@ -577,7 +590,7 @@ def run_ours(args, wl):
             "layer_us": ms_step * 1e3, "proj_us": proj_us, "layer_hbm_frac": layer_frac,
             "layer_algorithmic_bytes": layer_bytes,
             "slora": slora, "nfs": nfs, "collectives": collectives, "tp_emulated_1gpu": tp_emulated,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "decode_step": decode_step,
             "gpu_launches": launches * args.steps, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -588,6 +601,77 @@ def run_ours(args, wl):
 
         dist.destroy_process_group()
     return 0
+
+
+def time_decode_step(bd, torch, wl, n, rank, dev, comm, steps, warmup, layers, local_only=False):
+    """the whole decode step: `layers` decoder layers, each QKV -> [attention
+    placeholder] -> O -> gate_up -> [SiLU*up placeholder] -> down, chained through their REAL inputs (each
+    projection reads the previous one's output) in one CUDA graph with programmatic dependent launch.
+    Placeholders (the sharding method does not touch them): O reads the q slice of QKV's output,
+    down reads the gate slice of gate_up's output (contiguous views at T = 1); no residual, norm or KV cache.
+    Every layer has its own base weights and its own rank-r adapter (slot = layer in one pool per
+    projection).  local_only: device-local work of rank 0 of an N-way TP group on one GPU (row layers as
+    partials, no all-reduce).  Returns us per decode step (= per output token at batch 1)."""
+    import synth
+
+    T = wl["T"]
+    if T != 1:
+        return None
+    projs = synth.arch_projections(wl["arch"])
+    r = wl["ranks"][0]
+    s = synth.rs_scale(16.0, r, n, "bd")
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321)
+    pools, Ws, Ys, wss = [], [], [], []
+    for p in projs:
+        par = bd.COLUMN if p.parallel == "column" else bd.ROW
+        pool = bd.bdlora_create_pool(par, bd.SHARD_BD, n, rank, p.d_in, p.d_out, layers, r, device=dev.index)
+        for layer in range(layers):
+            A, B = [], []
+            for dj in p.d_out:
+                if p.parallel == "column":
+                    A.append((torch.randn(p.d_in, r, generator=gen, device=dev) / math.sqrt(p.d_in)).to(torch.bfloat16))
+                    B.append((torch.randn(r // n, dj, generator=gen, device=dev) / (s * math.sqrt(r / n))).to(torch.bfloat16))
+                else:
+                    A.append((torch.randn(p.d_in, r // n, generator=gen, device=dev) / math.sqrt(p.d_in)).to(torch.bfloat16))
+                    B.append((torch.randn(r, dj, generator=gen, device=dev) / (s * math.sqrt(r / n))).to(torch.bfloat16))
+            bd.bdlora_load_adapter(pool, layer, r, s, A, B)
+        pools.append(pool)
+        Ws.append([(torch.randn(pool.m_loc, pool.k_loc, generator=gen, device=dev) / math.sqrt(p.d_in)).to(torch.bfloat16)
+                   for _ in range(layers)])
+        Ys.append(torch.empty(T, pool.m_loc, dtype=torch.bfloat16, device=dev))
+        wss.append(bd.make_workspace(pool, T))
+    ids = [torch.full((T,), layer, dtype=torch.int32, device=dev) for layer in range(layers)]
+    x0 = torch.randn(T, pools[0].k_loc, generator=gen, device=dev).to(torch.bfloat16)
+    q_cols, gate_cols = pools[1].k_loc, pools[3].k_loc
+
+    def step(k):
+        x = x0 if k == 0 else Ys[3]
+        for layer in range(layers):
+            i = ids[layer]
+            bd.bdlora_column_forward(pools[0], x, Ws[0][layer], i, Ys[0], wss[0])
+            xo = Ys[0][:, :q_cols]  # attention placeholder: the q slice
+            if local_only or comm is None:
+                bd.bdlora_row_partial(pools[1], xo, Ws[1][layer], i, Ys[1], wss[1])
+            else:
+                bd.bdlora_row_forward(pools[1], comm, xo, Ws[1][layer], i, Ys[1], wss[1])
+            bd.bdlora_column_forward(pools[2], Ys[1], Ws[2][layer], i, Ys[2], wss[2])
+            xd = Ys[2][:, :gate_cols]  # SiLU(gate) * up placeholder: the gate slice
+            if local_only or comm is None:
+                bd.bdlora_row_partial(pools[3], xd, Ws[3][layer], i, Ys[3], wss[3])
+            else:
+                bd.bdlora_row_forward(pools[3], comm, xd, Ws[3][layer], i, Ys[3], wss[3])
+            x = Ys[3]
+
+    for w in range(warmup):
+        step(1)
+    torch.cuda.synchronize()
+    ms = graph_time(torch, step, steps, lambda: None)
+    for pool in pools:
+        pool.close()
+    del Ws
+    torch.cuda.empty_cache()
+    return ms / steps * 1e3
 
 
 def time_layer_local(bd, torch, layer, ids, steps, warmup, tpn):
@@ -638,11 +722,15 @@ def main():
     ap.add_argument("--skip-slora", action="store_true", help="skip the S-LoRA and NFS-LoRA comparison legs")
     ap.add_argument("--skip-tp-emulation", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--decode-layers", type=int, default=None,
+                    help="layers of the whole-decode-step leg (batch-1 workloads; default: the model's depth; 0 = off)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: --warmup < 3 violates the timing rules; using 3")
         args.warmup = 3
     wl = WORKLOADS[args.workload]
+    if args.decode_layers is None:
+        args.decode_layers = {"llama-3.1-8b": 32}.get(wl["arch"], 0)  # 70B x 80 layers at TP1 would not fit beside the rest
     world, _, _ = dist_env()
     if world != args.gpus:
         log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; TP degree follows WORLD_SIZE")
