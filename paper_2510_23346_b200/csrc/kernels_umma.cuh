@@ -1187,8 +1187,8 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
   using S = UmmaSmem<BN>;
   UmmaParams p1 = p0;
   p1.nstages = std::min(S::kStages, umma_stage_cap(p0.T));
-  if (MODE == 0 && p1.cluster > 1) {
-    // every cluster must be co-resident in one wave (one CTA per SM); otherwise the global fix-up
+  while (MODE == 0 && p1.cluster > 1) {
+    // every cluster must be co-resident in one wave (one CTA per SM)
     static int max_clusters[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
     int& mc = max_clusters[p1.cluster];
     if (mc < 0) {
@@ -1196,7 +1196,7 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
                                S::kBytes) != cudaSuccess)
         return 2;
       cudaLaunchConfig_t qc = {};
-      qc.gridDim = dim3(p0.grid);
+      qc.gridDim = dim3(p1.grid);
       qc.blockDim = dim3(kUmmaThreads);
       qc.dynamicSmemBytes = S::kBytes;
       cudaLaunchAttribute ca[1];
@@ -1211,14 +1211,26 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
         mc = 0;
       }
     }
-    if ((long long)mc * p1.cluster < p0.grid) p1.cluster = 1;
-    // the K-local LoRA adds a 2 KB A box to every k-block: worth it only where the tail dominates (cluster
-    // reduce, short K segments -- measured alone: 8B O (16 k-blocks/CTA) -1.5 us but +1 us in the layer chain, 8B down (56) +5 us); otherwise
-    // the grid-wide shrink hides under the stream
-    if (p1.cluster == 1 || p1.k_blocks / p1.cluster > local_max_kb()) p1.local = 0;
+    const int tiles = p1.grid / p1.cluster;
+    const bool fits = (long long)mc >= tiles;
     if (getenv("BDLORA_DEBUG"))
-      fprintf(stderr, "[bdlora] umma BN=%d grid=%d cluster=%d (max active clusters %d) -> %d\n", BN, p0.grid,
-              p0.cluster, mc, p1.cluster);
+      fprintf(stderr, "[bdlora] umma BN=%d tiles=%d cluster=%d (max active clusters %d) fits=%d\n", BN, tiles,
+              p1.cluster, mc, (int)fits);
+    if (fits) break;
+    const char* shrink = getenv("BDLORA_CLUSTER_SHRINK");
+    if (shrink && shrink[0] == '0') {
+      p1.cluster = 1;  // keep the split, global fix-up
+      break;
+    }
+    // a smaller cluster: the tile split s shrinks with it (fewer, longer K segments per CTA)
+    p1.cluster -= 1;
+    p1.grid = tiles * p1.cluster;
+  }
+  if (MODE == 0 && p0.cluster > 1) {
+    // the K-local LoRA adds a 2 KB A box to every k-block: worth it only where the tail dominates (cluster
+    // reduce, short K segments -- measured alone: 8B O (16 k-blocks/CTA) -1.5 us but +1 us in the layer chain,
+    // 8B down (56) +5 us); otherwise the grid-wide shrink hides under the stream
+    if (p1.cluster == 1 || p1.k_blocks / p1.cluster > local_max_kb()) p1.local = 0;
   }
   static bool attr_set = false;
   if (!attr_set) {
@@ -1228,7 +1240,7 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p0.grid);
+  cfg.gridDim = dim3(p1.grid);
   cfg.blockDim = dim3(kUmmaThreads);
   cfg.dynamicSmemBytes = S::kBytes;
   cfg.stream = st;

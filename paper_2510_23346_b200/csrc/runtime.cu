@@ -511,6 +511,7 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+  if (const char* cap = getenv("BDLORA_GRID_CAP")) sms = std::max(1, std::min(sms, atoi(cap)));  // tuning only
   p->num_sms = sms;
   cudaError_t e1 = cudaMalloc(&p->arena, std::max<int64_t>(p->arena_elems, 8) * 2);
   cudaError_t e2 = cudaMalloc(&p->d_tab, sizeof(SlotEntry) * d.capacity);
