@@ -119,6 +119,8 @@ struct UmmaSmem {
   static constexpr int kBytes = kPreBOff + kPreBBytes + 1024;        // + alignment slack
   // the shrink MMA reads 128 rows (16 KB) from a stage's A box: rows 16..127 must stay inside the allocation
   static_assert(kBytes <= 232448, "exceeds 227 KB of dynamic shared memory per CTA");
+  static_assert(BN > 64 || kPartBytes > 0 || kStages * kWBytes >= (kUmmaBM + 8) * BN * 4,
+                "cluster split-K slots must fit in the weight rings");
   static_assert(!kHasA || kStages * (kWBytes + kXBytes) + kStages * kABytes + 16384 <= kBytes - 1024,
                 "shrink MMA window leaves the shared-memory allocation");
 };
@@ -154,6 +156,9 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   float* s_v = (float*)(smem + S::kVOff);        // [kVFloats] v rows of the current 16-token chunk
   float* s_preb = (float*)(smem + S::kPreBOff);  // decode: [16][128] B rows of each thread's column (parked)
   float* s_part = (float*)(smem + S::kPartOff);  // cluster split-K partial slots
+  // cluster split-K partial slots: dedicated (decode) or the weight rings once every mainloop is done
+  constexpr bool kSlotsInRing = S::kPartBytes == 0;
+  float* s_slots = kSlotsInRing ? reinterpret_cast<float*>(sW) : s_part;
   float* s_vst = (float*)(smem + S::kVStOff);    // tensor-core expand: [C][tv][J][Rc] v of the token tile
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -822,6 +827,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         if (u == u_lo) UMMA_TRACE(5);
         UMMA_TRACE(6);
       }
+      if (kSlotsInRing && !whole && p.cluster > 1) {
+        // the partial slots live in the (then idle) weight rings: wait until every contributor of the
+        // tile has finished its mainloop before anyone pushes
+        ptx::cluster_arrive();
+        ptx::cluster_wait();
+      }
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       if (local && la >= 0) {
         // this segment's v_seg: TMEM lanes k < r/N of the shrink accumulator (warp of lane quarter 0) -> smem
@@ -888,7 +899,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             const int owner = ((row + 1) * s - 1) / kUmmaBM;
             const int rr = row - (owner * kUmmaBM) / s;
             const uint32_t dst =
-                ptx::mapa(ptx::smem_u32(s_part + ((size_t)(crank * nr_max + rr) * BN + c0)), (uint32_t)owner);
+                ptx::mapa(ptx::smem_u32(s_slots + ((size_t)(crank * nr_max + rr) * BN + c0)), (uint32_t)owner);
 #pragma unroll
             for (int i = 0; i < 16; i += 4) ptx::st_dsmem_f4(dst + i * 4, f[i], f[i + 1], f[i + 2], f[i + 3]);
           } else {
@@ -914,7 +925,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         const int s = p.cluster, nr_max = (kUmmaBM + s - 1) / s;
         const int r_lo = (crank * kUmmaBM) / s, r_hi = ((crank + 1) * kUmmaBM) / s, nr = r_hi - r_lo;
         const int nq = (tv + 3) / 4;
-        const float* sp = s_part;
+        const float* sp = s_slots;
         for (int f = etid; f < nr * nq; f += 128) {
           const int rr = f % nr, qd = f / nr;
           float4 y = *reinterpret_cast<const float4*>(sp + (size_t)rr * BN + qd * 4);
@@ -1060,9 +1071,13 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
   }
 
-  if (MODE == 0 && p.cluster > 1 && warp < 2) {  // the epilogue's cluster barrier counts every thread
+  if (MODE == 0 && p.cluster > 1 && warp < 2) {  // the epilogue's cluster barriers count every thread
     ptx::cluster_arrive();
     ptx::cluster_wait();
+    if (kSlotsInRing) {
+      ptx::cluster_arrive();
+      ptx::cluster_wait();
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -1310,7 +1325,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
     long long s = std::max<long long>(1, std::min<long long>(num_sms / tiles, p.k_blocks / 8));
     // cluster split-K (the s contributors of a tile reduce through DSMEM): cheap fix-up, so split finer
     const long long sc = std::min<long long>(8, std::min<long long>(num_sms / tiles, p.k_blocks / 4));
-    if (cluster_splitk_enabled() && BN == 16 && sc >= 2) {
+    if (cluster_splitk_enabled() && BN <= 64 && sc >= 2) {
       s = sc;
       p.cluster = (int)sc;
     }
