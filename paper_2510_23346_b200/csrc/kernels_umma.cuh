@@ -1360,7 +1360,8 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.fuse = v_fused ? 1 : 0;
   p.v_out = v_fused;
   p.rs_max = rs_max;
-  p.tcx = (v_fused || !tensor_expand_enabled()) ? 0 : tcx;
+  // decode-sized token tiles (BN = 16) expand on the CUDA cores; larger fused batches on the tensor cores
+  p.tcx = (!tensor_expand_enabled() || (v_fused && BN == 16)) ? 0 : tcx;
   if (v_fused) p.v = v_fused;
   p.pdl = pdl;
   p.trace = g_umma_trace;

@@ -141,7 +141,11 @@ struct WsLayout {
   size_t off_counters, off_v, off_part, off_umma, off_route, off_shrink, total;
 };
 
-constexpr int kTcShrinkMinT = 17;  // tensor-core shrink above decode sizes (T <= 16: fused CUDA-core shrink)
+constexpr int kTcShrinkMinT = 17;  // phases API: tensor-core shrink above decode sizes
+// forwards: one kernel (grid-wide shrink inside the GEMM) up to 16 tokens.  Measured at T = 64 (70B, A/B
+// with BDLORA_FUSED_MAX_T=64): the grid-wide CUDA-core shrink loses to route + tensor-core shrink both for one
+// adapter (bs64 TP8 layer 196 vs 143 us) and for ~50 adapters (multi-tenant TP8 322 vs 238 us)
+constexpr int kFusedMaxT = 16;
 
 // Upper bound of the tensor-core shrink's 16-row A boxes for a batch of T tokens (0 = not eligible).
 int tc_items_max(const bdlora_pool* p, int64_t T) {
@@ -151,6 +155,16 @@ int tc_items_max(const bdlora_pool* p, int64_t T) {
   const int64_t items = groups * p->g.J * ((p->rs_max + 15) / 16);
   if (items > bdl::kRouteMaxItems) return 0;
   return (int)items;
+}
+
+// Largest batch served by the single-kernel forward (BDLORA_FUSED_MAX_T overrides; tuning / A-B)
+int fused_max_t() {
+  static int v = -1;
+  if (v < 0) {
+    const char* s = getenv("BDLORA_FUSED_MAX_T");
+    v = s ? std::max(0, std::min(atoi(s), bdl::kFuseMaxT)) : kFusedMaxT;
+  }
+  return v;
 }
 
 WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
@@ -812,13 +826,13 @@ int bdlora_base_expand(bdlora_pool* p, const void* X, int64_t T, const void* W, 
 static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y, void* ws,
                     cudaStream_t st) {
   float* v = ws_v(p, ws, T);
-  if (bdl::umma_eligible(p->g, (int)T) && T < kTcShrinkMinT) {
+  if (bdl::umma_eligible(p->g, (int)T) && T <= fused_max_t()) {
     // decode: ONE kernel -- the LoRA shrink runs inside it (K-local on the tensor cores for a single
     // adapter group, else in the epilogue warps) while the weights stream
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, (int)T, (const __nv_bfloat16*)W, ids, p->d_tab,
                               (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
-                              p->num_sms, st, g_pdl, v, p->rs_max, 0, p->amap_ok ? &p->amap : nullptr);
+                              p->num_sms, st, g_pdl, v, p->rs_max, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
     if (rc == 0) {
       count_launch();
       CU_TRY(cudaGetLastError());
