@@ -153,6 +153,18 @@ int bdlora_destroy_pool(bdlora_pool* pool);
 int bdlora_load_adapter(bdlora_pool* pool, int32_t slot, int32_t rank, float scale,
                         const void* const* A, const void* const* B, int32_t src_is_device,
                         bdlora_stream_t stream);
+/* Downward-compatible BD serving: an adapter TRAINED for N_h = n_blocks
+   devices (its compact B_1 / A_2 hold N_h diagonal blocks) served on tp_size = N_l devices, N_l | N_h.
+   Device i runs the work of the N_h-layout devices i*m .. (i+1)*m - 1 (m = N_h/N_l) -- "stacking the
+   computations of different devices": its A_1 / B_2 shards are the union of theirs (rank chunk
+   [i r/N_l, (i+1) r/N_l)), and its local B_1 (COLUMN) or A_2 (ROW) is block-diagonal with those m
+   blocks, stored densely with explicit zeros (the same kernels run it; the zeros cost (m-1)/m of the
+   B_1 / A_2 shard bytes -- B_1, A_2 are r/N_l x d/N_l, small next to the base weight).  Load format =
+   bdlora_load_adapter's BD format with N_h in place of N.  BD pools only (E_MODE); N_l | N_h, N_h | r and
+   N_h | d_out[j] (COLUMN) or d_in (ROW) (E_DIVISIBILITY).  n_blocks == tp_size = bdlora_load_adapter. */
+int bdlora_load_adapter_blocks(bdlora_pool* pool, int32_t slot, int32_t rank, float scale,
+                               const void* const* A, const void* const* B, int32_t n_blocks,
+                               int32_t src_is_device, bdlora_stream_t stream);
 int bdlora_unload_adapter(bdlora_pool* pool, int32_t slot);
 /* Resident adapter bytes (compact shards) and arena capacity in bytes.                          */
 int bdlora_pool_bytes(const bdlora_pool* pool, int64_t* resident, int64_t* arena);

@@ -209,6 +209,31 @@ def row_partial_bd(X_full: np.ndarray, W: np.ndarray, adapter_inputs: Dict[int, 
     return P
 
 
+def row_partial_bd_blocks(X_full: np.ndarray, W: np.ndarray, adapter_inputs: Dict[int, dict], ids: np.ndarray,
+                          n_blocks: int, n_dev: int, i: int) -> np.ndarray:
+    """Downward-compatible BD-LoRA row partial: an adapter trained with N_h = n_blocks diagonal
+    blocks served on N_l = n_dev devices.  Device i holds the row shard i of X, W (d_in/N_l rows) and
+    runs the N_h-layout devices i*m .. (i+1)*m - 1 (m = N_h/N_l):
+
+        P_i = X^i W^i + s X^i (A_2[rows i, :] B_2),   A_2 = bd_expand_stacked(compact, N_h)
+
+    i.e. the dense block-diagonal A_2 of the TRAINING layout restricted to this device's rows.  Pinned
+    to the sum of the N_h-layout partials `row_partial_bd(..., N_h, d)` over d in the group and, summed
+    over i, to `row_layer(..., "bd", N_h)` (tests/test_oracle_pins.py)."""
+    X_full = np.asarray(X_full, dtype=np.float64)
+    d_in = X_full.shape[1]
+    bi = d_in // n_dev
+    Xi = X_full[:, i * bi:(i + 1) * bi]
+    P = Xi @ np.asarray(W[i * bi:(i + 1) * bi, :], dtype=np.float64)
+    for a in sorted(set(int(v) for v in np.asarray(ids).tolist()) - {-1}):
+        ad = adapter_inputs[a]
+        A = bd_expand_stacked(np.asarray(ad["A"][0], dtype=np.float64), n_blocks)
+        B = np.asarray(ad["B"][0], dtype=np.float64)
+        rows = np.nonzero(np.asarray(ids) == a)[0]
+        P[rows] += float(ad["scale"]) * (Xi[rows] @ (A[i * bi:(i + 1) * bi, :] @ B))
+    return P
+
+
 def row_partial_nfs(X_full: np.ndarray, W: np.ndarray, adapter_inputs: Dict[int, dict], ids: np.ndarray,
                     n: int, i: int) -> np.ndarray:
     """Per-device partial of an NFS-LoRA row layer ("adapters A_1 and B_2 are not sharded

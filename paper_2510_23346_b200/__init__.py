@@ -28,7 +28,7 @@ __all__ = [
     "bdlora_load_adapter", "bdlora_unload_adapter", "bdlora_pool_bytes", "bdlora_pool_geometry",
     "bdlora_workspace_bytes", "bdlora_build_segments", "bdlora_column_forward", "bdlora_row_partial",
     "bdlora_row_forward", "slora_column_forward", "slora_row_forward", "bdlora_lora_shrink",
-    "bdlora_base_expand", "bdlora_v_elems", "make_workspace", "bdlora_set_decode_lora",
+    "bdlora_base_expand", "bdlora_v_elems", "make_workspace", "bdlora_set_decode_lora", "bdlora_load_adapter_blocks",
 ]
 
 
@@ -199,29 +199,40 @@ def bdlora_destroy_pool(pool: Pool) -> None:
     pool.close()
 
 
-def bdlora_load_adapter(pool: Pool, slot: int, rank: int, scale: float, A: Sequence, B: Sequence,
-                        stream=None) -> None:
-    """A, B: per-slice bf16 torch tensors in the load format of include/bdlora.h (all on the pool's
-    device, or all on the CPU)."""
+def _factor_ptrs(pool: Pool, A: Sequence, B: Sequence):
     torch = _torch()
     J = pool.desc.n_slices
     if len(A) != J or len(B) != J:
         raise ValueError(f"need {J} A and {J} B factors")
     on_dev = None
-    keep = []
     for t in list(A) + list(B):
         _need(t, "factor", dtype=torch.bfloat16)
-        dev = t.is_cuda
+        if not t.is_contiguous():
+            raise ValueError("factors must be contiguous (row-major)")
         if on_dev is None:
-            on_dev = dev
-        elif on_dev != dev:
+            on_dev = t.is_cuda
+        elif on_dev != t.is_cuda:
             raise ValueError("factors must be all host or all device tensors")
-        keep.append(t)
     pa = (ctypes.c_void_p * J)(*[a.data_ptr() for a in A])
     pb = (ctypes.c_void_p * J)(*[b.data_ptr() for b in B])
-    call("bdlora_load_adapter", pool.handle, slot, rank, ctypes.c_float(scale), pa, pb, 1 if on_dev else 0,
-         _stream(stream) if on_dev else _stream(stream))
-    del keep
+    return pa, pb, 1 if on_dev else 0
+
+
+def bdlora_load_adapter(pool: Pool, slot: int, rank: int, scale: float, A: Sequence, B: Sequence,
+                        stream=None) -> None:
+    """A, B: per-slice bf16 torch tensors in the load format of include/bdlora.h (all on the pool's
+    device, or all on the CPU)."""
+    pa, pb, on_dev = _factor_ptrs(pool, A, B)
+    call("bdlora_load_adapter", pool.handle, slot, rank, ctypes.c_float(scale), pa, pb, on_dev, _stream(stream))
+
+
+def bdlora_load_adapter_blocks(pool: Pool, slot: int, rank: int, scale: float, A: Sequence, B: Sequence,
+                               n_blocks: int, stream=None) -> None:
+    """Downward-compatible BD serving: factors trained with n_blocks = N_h diagonal blocks,
+    served on this pool's tp_size = N_l devices (include/bdlora.h)."""
+    pa, pb, on_dev = _factor_ptrs(pool, A, B)
+    call("bdlora_load_adapter_blocks", pool.handle, slot, rank, ctypes.c_float(scale), pa, pb, int(n_blocks), on_dev,
+         _stream(stream))
 
 
 def bdlora_unload_adapter(pool: Pool, slot: int) -> None:

@@ -44,6 +44,8 @@ SIGNATURES = {
     "bdlora_destroy_pool": (c_int, [c_vp]),
     "bdlora_load_adapter": (c_int, [c_vp, c_i32, c_i32, c_f32, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i32, c_vp]),
     "bdlora_unload_adapter": (c_int, [c_vp, c_i32]),
+    "bdlora_load_adapter_blocks": (c_int, [c_vp, c_i32, c_i32, c_f32, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i32,
+                                           c_i32, c_vp]),
     "bdlora_pool_bytes": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
     "bdlora_pool_geometry": (c_int, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "bdlora_workspace_bytes": (c_int, [c_vp, c_i64, ctypes.POINTER(c_size)]),

@@ -324,10 +324,12 @@ __global__ void __launch_bounds__(256) gemv_lora_kernel(const __nv_bfloat16* __r
 }
 
 // ------------------------------------------------------------------------------------------------
-// Loader: dst = (transpose ? src[r0:r0+nr, c0:c0+nc]^T : src[r0:r0+nr, c0:c0+nc]), src row-major ld.
+// Loader: dst = (transpose ? src[r0:r0+nr, c0:c0+nc]^T : src[r0:r0+nr, c0:c0+nc]), src row-major ld,
+// dst row-major with leading dimension ldd (0 = packed: nc, or nr when transposed).
 // ------------------------------------------------------------------------------------------------
 __global__ void gather_kernel(const uint16_t* __restrict__ src, long long ld, int r0, int c0, int nr, int nc,
-                              int transpose, uint16_t* __restrict__ dst) {
+                              int transpose, uint16_t* __restrict__ dst, long long ldd) {
+  if (ldd == 0) ldd = transpose ? nr : nc;
   __shared__ uint16_t tile[32][33];
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;  // bx over columns, by over rows of the sub-block
   for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
@@ -338,12 +340,12 @@ __global__ void gather_kernel(const uint16_t* __restrict__ src, long long ld, in
   if (!transpose) {
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
       const int r = by + yy, c = bx + threadIdx.x;
-      if (r < nr && c < nc) dst[(long long)r * nc + c] = tile[yy][threadIdx.x];
+      if (r < nr && c < nc) dst[(long long)r * ldd + c] = tile[yy][threadIdx.x];
     }
   } else {
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
       const int c = bx + yy, r = by + threadIdx.x;  // dst row = c, dst col = r
-      if (r < nr && c < nc) dst[(long long)c * nr + r] = tile[threadIdx.x][yy];
+      if (r < nr && c < nc) dst[(long long)c * ldd + r] = tile[threadIdx.x][yy];
     }
   }
 }

@@ -591,18 +591,44 @@ static void arena_free(bdlora_pool* p, int64_t off, int64_t elems) {
 }
 
 static int gather_to(const uint16_t* src, int64_t ld, int r0, int c0, int nr, int nc, int transpose, uint16_t* dst,
-                     cudaStream_t st) {
+                     cudaStream_t st, int64_t ldd = 0) {
   if (nr == 0 || nc == 0) return BDLORA_OK;
   dim3 grid((nc + 31) / 32, (nr + 31) / 32);
-  bdl::gather_kernel<<<grid, dim3(32, 8), 0, st>>>(src, ld, r0, c0, nr, nc, transpose, dst);
+  bdl::gather_kernel<<<grid, dim3(32, 8), 0, st>>>(src, ld, r0, c0, nr, nc, transpose, dst, ldd);
   count_launch();
   CU_TRY(cudaGetLastError());
   return BDLORA_OK;
 }
 
+static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float scale, const void* const* A,
+                             const void* const* B, int32_t src_is_device, bdlora_stream_t stream, int nb);
+
 int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale, const void* const* A,
                         const void* const* B, int32_t src_is_device, bdlora_stream_t stream) {
   ST_TRY(check_pool(p));
+  return load_adapter_impl(p, slot, rank, scale, A, B, src_is_device, stream, p->d.tp_size);
+}
+
+int bdlora_load_adapter_blocks(bdlora_pool* p, int32_t slot, int32_t rank, float scale, const void* const* A,
+                               const void* const* B, int32_t n_blocks, int32_t src_is_device, bdlora_stream_t stream) {
+  ST_TRY(check_pool(p));
+  const auto& d = p->d;
+  if (d.sharding != BDLORA_SHARD_BD) return fail(BDLORA_E_MODE, "bdlora_load_adapter_blocks needs a BD pool");
+  if (n_blocks < d.tp_size || n_blocks % d.tp_size)
+    return fail(BDLORA_E_DIVISIBILITY, "n_blocks %d must be a multiple of tp_size %d (P:499-507)", n_blocks, d.tp_size);
+  if (rank % n_blocks) return fail(BDLORA_E_DIVISIBILITY, "rank %d not divisible by n_blocks %d", rank, n_blocks);
+  if (d.parallel == BDLORA_COLUMN) {
+    for (int j = 0; j < d.n_slices; ++j)
+      if (d.d_out[j] % n_blocks)
+        return fail(BDLORA_E_DIVISIBILITY, "d_out[%d] = %d not divisible by n_blocks %d", j, d.d_out[j], n_blocks);
+  } else if (d.d_in % n_blocks) {
+    return fail(BDLORA_E_DIVISIBILITY, "d_in %d not divisible by n_blocks %d", d.d_in, n_blocks);
+  }
+  return load_adapter_impl(p, slot, rank, scale, A, B, src_is_device, stream, n_blocks);
+}
+
+static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float scale, const void* const* A,
+                             const void* const* B, int32_t src_is_device, bdlora_stream_t stream, int nb) {
   const auto& d = p->d;
   if (slot < 0 || slot >= d.capacity) return fail(BDLORA_E_CAPACITY, "slot %d out of range [0,%d)", slot, d.capacity);
   if (rank < 1 || rank > d.max_rank) return fail(BDLORA_E_CAPACITY, "rank %d out of range [1,%d]", rank, d.max_rank);
@@ -677,12 +703,23 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
       e.offA[j] = cur;
       rc = gather_to(sa, rank, 0, i * (rank / N), d.d_in, rank / N, 1, p->arena + cur, st);
       cur += (int64_t)rs * K;
-    } else if (d.sharding == BDLORA_SHARD_BD) {
+    } else if (d.sharding == BDLORA_SHARD_BD && nb == N) {
       // A_2 compact d_in x r/N, blocks stacked; diagonal block i = rows [i*d_in/N, ...)
       rc = src_ptr(A[0], (int64_t)d.d_in * (rank / N), &sa);
       if (rc) break;
       e.offA[0] = cur;
       rc = gather_to(sa, rank / N, i * K, 0, K, rank / N, 1, p->arena + cur, st);
+      cur += (int64_t)rs * K;
+    } else if (d.sharding == BDLORA_SHARD_BD) {
+      // downward-compatible: compact d_in x r/N_h with N_h stacked blocks; this device runs the
+      // blocks b = i*m + bb (m = N_h/N): the local A_2 is block-diagonal, stored transposed [r/N, d_in/N]
+      const int m = nb / N, rb = rank / nb, kb = d.d_in / nb;
+      rc = src_ptr(A[0], (int64_t)d.d_in * rb, &sa);
+      if (rc) break;
+      e.offA[0] = cur;
+      if (cudaMemsetAsync(p->arena + cur, 0, (size_t)rs * K * 2, st) != cudaSuccess) rc = fail(BDLORA_E_CUDA, "memset");
+      for (int bb = 0; bb < m && rc == BDLORA_OK; ++bb)
+        rc = gather_to(sa, rb, (i * m + bb) * kb, 0, kb, rb, 1, p->arena + cur + (int64_t)bb * rb * K + bb * kb, st, K);
       cur += (int64_t)rs * K;
     } else {
       // S-LoRA / NFS row: A_2 d_in x r row-sharded: rows [i*d_in/N, ...)
@@ -694,12 +731,22 @@ int bdlora_load_adapter(bdlora_pool* p, int32_t slot, int32_t rank, float scale,
     }
     if (rc) break;
     // ---- B_j -> [re, w] ----
-    if (d.parallel == BDLORA_COLUMN && d.sharding == BDLORA_SHARD_BD) {
+    if (d.parallel == BDLORA_COLUMN && d.sharding == BDLORA_SHARD_BD && nb == N) {
       // compact (r/N) x d_out_j, blocks side by side; diagonal block i = columns [i*w, ...)
       rc = src_ptr(B[j], (int64_t)(rank / N) * dout, &sb);
       if (rc) break;
       e.offB[j] = curB;
       rc = gather_to(sb, dout, 0, i * w, rank / N, w, 0, p->arena + curB, st);
+    } else if (d.parallel == BDLORA_COLUMN && d.sharding == BDLORA_SHARD_BD) {
+      // downward-compatible: compact (r/N_h) x d_out_j with N_h blocks side by side; the local
+      // B_1 [r/N, d_out_j/N] is block-diagonal with this device's m = N_h/N blocks
+      const int m = nb / N, rb = rank / nb, cb = dout / nb;
+      rc = src_ptr(B[j], (int64_t)rb * dout, &sb);
+      if (rc) break;
+      e.offB[j] = curB;
+      if (cudaMemsetAsync(p->arena + curB, 0, (size_t)re * w * 2, st) != cudaSuccess) rc = fail(BDLORA_E_CUDA, "memset");
+      for (int bb = 0; bb < m && rc == BDLORA_OK; ++bb)
+        rc = gather_to(sb, dout, 0, (i * m + bb) * cb, rb, cb, 0, p->arena + curB + (int64_t)bb * rb * w + bb * cb, st, w);
     } else if (d.parallel == BDLORA_COLUMN) {
       // S-LoRA / NFS column: B_1 r x d_out_j column-sharded
       rc = src_ptr(B[j], (int64_t)rank * dout, &sb);

@@ -1,0 +1,36 @@
+"""The schedule knobs of the GEMM (read once per process from the environment) change only scheduling,
+never values: re-run a parity subset against the fp64 oracle in a subprocess under each alternative
+schedule -- global split-K fix-up instead of the cluster/DSMEM reduce, no cluster shrinking, stream-K
+over every SM, the single-kernel forward at T = 64 (grid-wide shrink + tensor-core expand), the
+CUDA-core expand, no K-local LoRA."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUBSET = ("column_bd_8b_qkv or row_bd_8b_down or decode_lora_schedules or integer_mode or multitenant "
+          "or prefill_token_tiles or nfs_row")
+
+VARIANTS = {
+    "global_fixup": {"BDLORA_CLUSTER": "0"},
+    "no_cluster_shrink": {"BDLORA_CLUSTER_SHRINK": "0"},
+    "streamk_all_sms": {"BDLORA_STREAMK_CTAS": "148"},
+    "fused_t64": {"BDLORA_FUSED_MAX_T": "64"},
+    "cuda_core_expand": {"BDLORA_TC_EXPAND": "0"},
+    "no_k_local": {"BDLORA_LOCAL": "0"},
+}
+
+
+@pytest.mark.parametrize("name", sorted(VARIANTS))
+def test_parity_under_schedule_variant(name):
+    env = dict(os.environ, **VARIANTS[name])
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"), "-m", "gpu",
+                        "-x", "-q", "-k", SUBSET, "-p", "no:cacheprovider"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    tail = "\n".join((r.stdout + r.stderr).strip().splitlines()[-15:])
+    assert r.returncode == 0, f"{name} {VARIANTS[name]}:\n{tail}"
+    assert " passed" in tail, tail

@@ -274,6 +274,44 @@ def test_nfs_column_and_row_bruteforce(n):
     assert np.array_equal(acc_, y)
 
 
+# ----------------------------------------------------------------------------- downward-compatible BD
+
+@pytest.mark.parametrize("nh,nl", [(4, 2), (4, 1), (8, 2)])
+def test_downward_compatible_bd_bruteforce(nh, nl):
+    """An adapter trained for N_h devices served on N_l | N_h devices: device i of N_l runs the N_h-layout
+    devices i*m..(i+1)*m-1 ("stacking the computations of different devices").  Column: its
+    output block is the concatenation (per slice) of those devices' pure-Python Alg. 2 outputs; row: its
+    partial is the sum of their Alg. 1 partials; both exactly on integers."""
+    rng = np.random.default_rng(60 + nh + nl)
+    m = nh // nl
+    d_out, ads = _tiny_bd(rng, "column", nh, d_in=8, d_out=(8, 16), r=8)
+    T, d_in = 5, 8
+    X = _int_mat(rng, (T, d_in))
+    W = _int_mat(rng, (d_in, sum(d_out)))
+    ids = np.array([0, 2, -1, 1, 0], dtype=np.int32)
+    full = ol.column_layer(X, W, d_out, ads, ids, "bd", nh)
+    for i in range(nl):
+        got = ol.column_device_output(full, nl, i)
+        parts, c0 = [], 0
+        for j, dj in enumerate(d_out):   # slice j of device i = the slice-j blocks of its m N_h-devices
+            for d in range(i * m, (i + 1) * m):
+                dev = _bf_column_device(X.tolist(), W.tolist(), d_out, ads, ids.tolist(), nh, d)
+                off = sum(dk // nh for dk in d_out[:j])
+                parts.append(dev[:, off:off + dj // nh])
+        assert np.array_equal(got, np.concatenate(parts, axis=1))
+    d_out_r, rads = _tiny_bd(rng, "row", nh, d_in=16, d_out=(6,), r=8)
+    Xr = _int_mat(rng, (T, 16))
+    Wr = _int_mat(rng, (16, 6))
+    y = ol.row_layer(Xr, Wr, rads, ids, "bd", nh)
+    acc_ = np.zeros_like(y)
+    for i in range(nl):
+        ref = sum(_bf_row_partial(Xr.tolist(), Wr.tolist(), rads, ids.tolist(), nh, d) for d in range(i * m, (i + 1) * m))
+        got = ol.row_partial_bd_blocks(Xr, Wr, rads, ids, nh, nl, i)
+        assert np.array_equal(got, ref)
+        acc_ += got
+    assert np.array_equal(acc_, y)
+
+
 # ----------------------------------------------------------------------------- P3 / P4 / P5
 
 def test_n1_bd_is_plain_lora():
