@@ -296,6 +296,69 @@ def test_nfs_integer_mode_bit_exact(dev, n, T):
         assert np.array_equal(got, ref), f"row rank {i}: {np.count_nonzero(got != ref)} mismatches"
 
 
+# ----------------------------------------------------------------------------- downward-compatible BD
+
+def _run_blocks(case, nl, i, dev):
+    """Pool with tp_size = nl loading case's N_h-format adapters through bdlora_load_adapter_blocks."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = case.proj
+    par = bd.COLUMN if proj.parallel == "column" else bd.ROW
+    pool = bd.bdlora_create_pool(par, bd.SHARD_BD, nl, i, proj.d_in, proj.d_out, case.capacity, case.max_rank)
+    for a, ad in case.adapters.items():
+        bd.bdlora_load_adapter_blocks(pool, a, ad.rank, ad.scale, [H.torch_bf16(x.bits) for x in ad.A],
+                                      [H.torch_bf16(x.bits) for x in ad.B], case.n)
+    X = H.torch_bf16(H.x_shard(case.X, proj, nl, i), dev)
+    W = H.torch_bf16(H.base_shard_T(case.W, proj, nl, i), dev)
+    ids = torch.from_numpy(case.ids).to(dev)
+    T = X.shape[0]
+    Y = torch.full((T, pool.m_loc), float("nan"), dtype=torch.bfloat16, device=dev)
+    ws = bd.make_workspace(pool, T)
+    (bd.bdlora_column_forward if par == bd.COLUMN else bd.bdlora_row_partial)(pool, X, W, ids, Y, ws)
+    torch.cuda.synchronize()
+    pool.close()
+    return Y
+
+
+@pytest.mark.parametrize("nh,nl", [(8, 1), (8, 2), (8, 4), (4, 2)])
+@pytest.mark.parametrize("T", [1, 37])
+def test_downward_compatible_serving(dev, nh, nl, T):
+    """Adapters trained for N_h devices served on N_l | N_h devices: column device blocks and
+    row partials vs the oracle of the N_h-block adapter read off in the N_l layout."""
+    qkv, down = synth.arch_projections("llama-3.1-8b")[0], synth.arch_projections("llama-3.1-8b")[3]
+    case = H.make_case(1500 + 10 * nh + nl + T, qkv, "bd", nh, T, ranks=[16, 32, 8])
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, qkv.d_out, case.oracle_adapters(), case.ids, "bd", nh)
+    for i in sorted({0, nl - 1}):
+        _assert_tol(_np(_run_blocks(case, nl, i, dev)), ol.column_device_output(ref_full, nl, i), f"col {nh}->{nl} dev {i}")
+    case = H.make_case(1600 + 10 * nh + nl + T, down, "bd", nh, T, ranks=[16, 32])
+    ads = case.oracle_adapters()
+    acc = None
+    for i in range(nl):
+        P = _np(_run_blocks(case, nl, i, dev))
+        _assert_tol(P, ol.row_partial_bd_blocks(case.X.f64, case.W.f64, ads, case.ids, nh, nl, i), f"row {nh}->{nl} dev {i}")
+        acc = P if acc is None else acc + P
+    _assert_tol(acc, ol.row_layer(case.X.f64, case.W.f64, ads, case.ids, "bd", nh), f"row {nh}->{nl} sum")
+
+
+def test_downward_compatible_integer_bit_exact(dev):
+    """P10 for downward-compatible serving: N_h = 8 adapters on N_l = 2, bit-identical to the oracle."""
+    col = synth.Projection("qkv", "column", 1024, (512, 256, 256))
+    case = H.make_case(1700, col, "bd", 8, 9, ranks=[8, 16, 32], integer=True)
+    ref_full = ol.column_layer(case.X.f64, case.W.f64, col.d_out, case.oracle_adapters(), case.ids, "bd", 8)
+    for i in range(2):
+        got, ref = _np(_run_blocks(case, 2, i, dev)), ol.bf16_round(ol.column_device_output(ref_full, 2, i))
+        assert np.array_equal(got, ref), f"dev {i}: {np.count_nonzero(got != ref)} mismatches"
+    row = synth.Projection("down", "row", 1024, (512,))
+    case = H.make_case(1701, row, "bd", 8, 9, ranks=[8, 16, 32], integer=True)
+    ads = case.oracle_adapters()
+    for i in range(2):
+        got = _np(_run_blocks(case, 2, i, dev))
+        ref = ol.bf16_round(ol.row_partial_bd_blocks(case.X.f64, case.W.f64, ads, case.ids, 8, 2, i))
+        assert np.array_equal(got, ref), f"row dev {i}: {np.count_nonzero(got != ref)} mismatches"
+
+
 # ----------------------------------------------------------------------------- P10 integer mode
 
 @pytest.mark.parametrize("sharding", ["bd", "slora"])
