@@ -204,6 +204,16 @@ int bdlora_row_partial(bdlora_pool* pool, const void* X, int64_t T, const void* 
 int bdlora_row_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
                        const int32_t* ids, void* Y, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
 
+/* Alg. 2 (a single column-parallel linear layer whose output is replicated): the column
+   forward above on every device, then the base model's all-gather -- still no LoRA collective.
+   Y [T, N * M_loc] bf16 = [Y_0 | Y_1 | ... | Y_{N-1}], the device blocks in rank order (for n_slices = 1
+   exactly the full output X W + s X A B; for stacked slices the blocks keep their [q_i | k_i | v_i] order).
+   The workspace (bdlora_workspace_bytes) holds the [N][T][M_loc] staging of the in-place ncclAllGather.
+   comm may be NULL iff tp_size == 1 (then it is bdlora_column_forward).  Pool: COLUMN + BD.          */
+int bdlora_column_forward_gather(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
+                                 const int32_t* ids, void* Y, void* workspace, size_t ws_bytes,
+                                 bdlora_stream_t stream);
+
 /* ---------------------------------------------------------------- S-LoRA comparison --------- */
 /* Column: v_i = s X A[:, chunk i] -> ncclAllGather -> v [T, r] -> Y_i = X W_i + v B[:, cols i].
    Same tensors as bdlora_column_forward; pool COLUMN + SLORA.  +1 all-gather (merged over the

@@ -22,7 +22,7 @@ SHARD_BD, SHARD_SLORA, SHARD_NFS = 0, 1, 2
 
 __all__ = [
     "COLUMN", "ROW", "SHARD_BD", "SHARD_SLORA", "SHARD_NFS", "nfs_column_forward", "nfs_row_partial",
-    "nfs_row_forward", "BdloraError", "Pool", "Comm",
+    "nfs_row_forward", "bdlora_column_forward_gather", "BdloraError", "Pool", "Comm",
     "bdlora_abi_version", "bdlora_device_check", "bdlora_kernel_launches", "bdlora_comm_unique_id", "bdlora_comm_init",
     "bdlora_comm_destroy", "bdlora_comm_stats", "bdlora_create_pool", "bdlora_destroy_pool",
     "bdlora_load_adapter", "bdlora_unload_adapter", "bdlora_pool_bytes", "bdlora_pool_geometry",
@@ -313,6 +313,21 @@ def bdlora_row_forward(pool: Pool, comm: Optional[Comm], X, W, ids, Y, ws, strea
     T = _check_fwd(pool, X, W, ids, Y, ws, pool.k_loc, pool.m_loc)
     call("bdlora_row_forward", pool.handle, _comm_ptr(comm), _ptr(X), T, _ptr(W), _ptr(ids), _ptr(Y), _ptr(ws),
          ws.numel(), _stream(stream))
+
+
+def bdlora_column_forward_gather(pool: Pool, comm: Optional[Comm], X, W, ids, Y, ws, stream=None) -> None:
+    """Alg. 2: column forward + all-gather; Y [T, N * M_loc] = device blocks in rank order."""
+    torch = _torch()
+    dev = pool.tdevice
+    _need(X, "X", dtype=torch.bfloat16, device=dev)
+    T = X.shape[0]
+    _need(X, "X", shape=(T, pool.k_loc))
+    _need(W, "W", dtype=torch.bfloat16, device=dev, shape=(pool.m_loc, pool.k_loc))
+    _need(ids, "ids", dtype=torch.int32, device=dev, shape=(T,))
+    _need(Y, "Y", dtype=torch.bfloat16, device=dev, shape=(T, pool.m_loc * pool.desc.tp_size))
+    _need(ws, "workspace", dtype=torch.uint8, device=dev)
+    call("bdlora_column_forward_gather", pool.handle, _comm_ptr(comm), _ptr(X), T, _ptr(W), _ptr(ids), _ptr(Y),
+         _ptr(ws), ws.numel(), _stream(stream))
 
 
 def slora_column_forward(pool: Pool, comm: Optional[Comm], X, W, ids, Y, ws, stream=None) -> None:

@@ -53,6 +53,7 @@ SIGNATURES = {
     "bdlora_column_forward": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "bdlora_row_partial": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "bdlora_row_forward": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "bdlora_column_forward_gather": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "slora_column_forward": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "slora_row_forward": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "nfs_column_forward": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),

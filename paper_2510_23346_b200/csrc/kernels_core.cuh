@@ -350,4 +350,15 @@ __global__ void gather_kernel(const uint16_t* __restrict__ src, long long ld, in
   }
 }
 
+// Alg. 2 all-gather output: G [N][T][M] (rank-major chunks) -> Y [T][N * M] (device blocks side by side).
+__global__ void interleave_chunks_kernel(const uint16_t* __restrict__ G, uint16_t* __restrict__ Y, int T, int M, int N) {
+  const long long total = (long long)N * T * M;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e % M);
+    const long long ct = e / M;
+    const int t = (int)(ct % T), c = (int)(ct / T);
+    Y[((long long)t * N + c) * M + m] = G[e];
+  }
+}
+
 }  // namespace bdl

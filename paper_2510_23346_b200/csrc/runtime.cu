@@ -138,7 +138,7 @@ constexpr int kMaxTiles = 8192;
 constexpr int kPartTokenSplits = 64;  // S x min(T, 8) <= 64 for the split-K GEMV
 
 struct WsLayout {
-  size_t off_counters, off_v, off_part, off_umma, off_route, off_shrink, total;
+  size_t off_counters, off_v, off_part, off_umma, off_route, off_shrink, off_gather, total;
 };
 
 constexpr int kTcShrinkMinT = 17;  // phases API: tensor-core shrink above decode sizes
@@ -184,6 +184,8 @@ WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   if (items > 0) o = align_up(o + sizeof(int) * bdl::RouteLayout::kWords, 256);
   L.off_shrink = o;
   if (items > 0) o = align_up(o + bdl::umma_shrink_workspace_bytes(items, (int)T, p->num_sms), 256);
+  L.off_gather = o;  // Alg. 2 all-gather staging: [N][T][M_loc] bf16 (column pools, N > 1)
+  if (p->d.parallel == BDLORA_COLUMN && p->d.tp_size > 1) o = align_up(o + (size_t)p->d.tp_size * T * p->g.M * 2, 256);
   L.total = o;
   return L;
 }
@@ -925,6 +927,32 @@ int bdlora_row_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t
     comm->counts[0] += 1;
     comm->counts[3] += (int64_t)n * 2;
   }
+  return BDLORA_OK;
+}
+
+// Alg. 2: column layer + the base model's all-gather of the device outputs -- replicated
+// Y [T, N * M_loc] = [Y_0 | Y_1 | ... | Y_{N-1}] (device blocks in rank order; for J = 1 the full output).
+int bdlora_column_forward_gather(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t T, const void* W,
+                                 const int32_t* ids, void* Y, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  ST_TRY(require_mode(p, BDLORA_COLUMN, BDLORA_SHARD_BD, "bdlora_column_forward_gather"));
+  ST_TRY(require_comm(p, comm, "bdlora_column_forward_gather"));
+  if (T == 0) return BDLORA_OK;
+  DeviceGuard dg(p->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = p->d.tp_size;
+  if (N == 1) return bd_local(p, X, T, W, ids, Y, ws, st);
+  // Alg. 2 lines 3-6 into this rank's chunk of the staging buffer, then an in-place all-gather (line 8)
+  __nv_bfloat16* G = (__nv_bfloat16*)((char*)ws + ws_layout(p, T).off_gather);
+  const size_t chunk = (size_t)T * p->g.M;
+  ST_TRY(bd_local(p, X, T, W, ids, G + chunk * p->d.tp_rank, ws, st));
+  // the base model's own collective: the LoRA counters of bdlora_comm_stats stay untouched
+  NC_TRY(ncclAllGather(G + chunk * p->d.tp_rank, G, chunk, ncclBfloat16, comm->nccl, st));
+  const size_t total = chunk * N;
+  bdl::interleave_chunks_kernel<<<(unsigned)std::min<size_t>((total + 255) / 256, 65535), 256, 0, st>>>(
+      (const uint16_t*)G, (uint16_t*)Y, (int)T, p->g.M, N);
+  count_launch();
+  CU_TRY(cudaGetLastError());
   return BDLORA_OK;
 }
 

@@ -359,6 +359,36 @@ def test_downward_compatible_integer_bit_exact(dev):
         assert np.array_equal(got, ref), f"row dev {i}: {np.count_nonzero(got != ref)} mismatches"
 
 
+# ----------------------------------------------------------------------------- Alg. 2
+
+def test_alg2_column_forward_gather(dev):
+    """Alg. 2: column forward + all-gather of the device outputs.  On one GPU: N = 1 (the gather is the
+    identity) vs the oracle's full output, and the N > 1 contract (a communicator is required)."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    proj = synth.tiny_pair()[0]
+    case = H.make_case(1800, proj, "bd", 1, 16, ranks=[8, 8, 16])
+    pool = H.make_pool(case, 0)
+    X, W, ids = H.device_inputs(case, 0, dev)
+    Y = torch.full((16, pool.m_loc), float("nan"), dtype=torch.bfloat16, device=dev)
+    ws = bd.make_workspace(pool, 16)
+    bd.bdlora_column_forward_gather(pool, None, X, W, ids, Y, ws)
+    torch.cuda.synchronize()
+    ref = ol.column_layer(case.X.f64, case.W.f64, proj.d_out, case.oracle_adapters(), case.ids, "bd", 1)[0]
+    _assert_tol(_np(Y), ref, "Alg. 2 N=1")
+    pool.close()
+    case2 = H.make_case(1801, proj, "bd", 2, 16, ranks=[8])
+    pool2 = H.make_pool(case2, 1)
+    X2, W2, ids2 = H.device_inputs(case2, 1, dev)
+    Y2 = torch.empty(16, 2 * pool2.m_loc, dtype=torch.bfloat16, device=dev)
+    with pytest.raises(bd.BdloraError) as ei:
+        bd.bdlora_column_forward_gather(pool2, None, X2, W2, ids2, Y2, bd.make_workspace(pool2, 16))
+    assert ei.value.code == 1
+    pool2.close()
+
+
 # ----------------------------------------------------------------------------- P10 integer mode
 
 @pytest.mark.parametrize("sharding", ["bd", "slora"])
