@@ -1151,11 +1151,34 @@ inline int streamk_ctas(int num_sms) {
 
 inline int umma_bn_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : T <= 64 ? 64 : T <= 128 ? 128 : 256; }
 
+// Token-tile width of the base GEMM.  Decode-sized batches take the smallest tile covering T.  For T > 64
+// (compute-bound) the width trades per-SM operand traffic -- FLOP per loaded byte ~ 128 BN / (128 + BN),
+// the kernel being bound by each SM's operand ingress -- against SM coverage and wave quantization:
+// e.g. 8B QKV at TP8 (6 row tiles, T = 1024): BN 256 gives 24 tiles (split 6 ways, 128 KB fp32 partials
+// each), BN 64 gives 96 whole tiles.  Never wider than umma_bn_for(T) (the workspace is sized for it).
+inline int umma_bn_for_gemm(int M, int T, int num_sms) {
+  const int bn0 = umma_bn_for(T);
+  if (T <= 64) return bn0;
+  const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM;
+  int best = bn0;
+  double best_eff = -1.0;
+  for (int bn = 64; bn <= bn0; bn *= 2) {
+    const long long tiles = (long long)m_tiles * ((T + bn - 1) / bn);
+    const long long waves = (tiles + num_sms - 1) / num_sms;
+    const double eff = (double)tiles / (double)(waves * num_sms) * (128.0 * bn) / (128.0 + bn);
+    if (eff > best_eff * 1.05) {  // ties -> the wider tile
+      best_eff = eff;
+      best = bn;
+    }
+  }
+  return best;
+}
+
 // Workspace: [sync: 3 ints, 256 B][tile counters][split-tile partials]
 inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
-  const int BN = umma_bn_for(T);
+  const int BN = umma_bn_for(T);  // the widest tile umma_bn_for_gemm may pick (partials)
   const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM;
-  const int n_tiles = (T + BN - 1) / BN;
+  const int n_tiles = (T + std::min(BN, 64) - 1) / std::min(BN, 64);  // the most tiles it may pick (counters)
   size_t part = (size_t)num_sms * 2 * BN * kUmmaBM * sizeof(float);
   size_t cnt = (size_t)m_tiles * n_tiles * sizeof(int);
   return 256 + ((cnt + 255) / 256) * 256 + part;
@@ -1304,7 +1327,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
                        int tcx = 0, const CUtensorMap* amap = nullptr) {
   if (!umma_eligible(g, T)) return 1;
   if (v_fused && T > kFuseMaxT) return 1;
-  const int BN = umma_bn_for(T);
+  const int BN = umma_bn_for_gemm(g.M, T, num_sms);
   UmmaParams p;
   p.M = g.M;
   p.K = g.K;
@@ -1323,6 +1346,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.cluster = 1;
   if (tiles <= num_sms) {
     long long s = std::max<long long>(1, std::min<long long>(num_sms / tiles, p.k_blocks / 8));
+    if (BN >= 128) s = 1;  // compute-bound tiles: a split would move >= 64 KB of fp32 partials per contributor
     // cluster split-K (the s contributors of a tile reduce through DSMEM): cheap fix-up, so split finer
     const long long sc = std::min<long long>(8, std::min<long long>(num_sms / tiles, p.k_blocks / 4));
     if (cluster_splitk_enabled() && BN <= 64 && sc >= 2) {
