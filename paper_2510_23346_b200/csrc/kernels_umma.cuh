@@ -876,7 +876,25 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           if (c0 > 0 && !p.tcx && !local)
             lora_chunk16(lr, n, t0 + c0, min(16, tv - c0), s_ids + c0, s_lead + c0, p.tab, p.arena, p.g, p.v, p.T,
                          &pre, s_v, S::kVFloats, etid);
-          if (n < p.M) {
+          if (tv >= 16 && (p.M & 7) == 0 && (reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) {
+            // multi-token chunk: transpose through shared memory (bf16 [16 tokens][128 columns]) so Y is
+            // written as whole token rows with 16-byte stores instead of 2-byte stores strided by M
+            uint16_t* st16 = reinterpret_cast<uint16_t*>(s_v);
+            ptx::named_bar_sync(1, 128);  // s_v free: LoRA staging readers / the previous chunk's copy-out done
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              st16[i * kUmmaBM + row] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r[i]) + lr[i]));
+            ptx::named_bar_sync(1, 128);
+            const int n0 = mt * kUmmaBM;
+#pragma unroll
+            for (int it = 0; it < 2; ++it) {
+              const int q = etid + it * 128, i = q >> 4, nn = n0 + (q & 15) * 8;
+              if (c0 + i < tv && nn < p.M) {
+                const uint4 val = *reinterpret_cast<const uint4*>(st16 + i * kUmmaBM + (q & 15) * 8);
+                *reinterpret_cast<uint4*>(p.Y + (size_t)(t0 + c0 + i) * p.M + nn) = val;
+              }
+            }
+          } else if (n < p.M) {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
               if (c0 + i < tv) p.Y[(size_t)(t0 + c0 + i) * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[i]) + lr[i]);
@@ -1413,7 +1431,9 @@ inline int umma_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, cons
                               const int* route, const CUtensorMap& amap, float* v_out, int items_max, void* ws,
                               int num_sms, cudaStream_t st, int pdl) {
   if (g.K % kUmmaBK != 0 || T < 1) return 1;
-  const int BN = umma_bn_for(T);
+  // few A boxes (rows) and many tokens: narrower token tiles give the shrink more CTAs (8B O prefill at TP8:
+  // BN 256 -> 4 CTAs, 30 us)
+  const int BN = umma_bn_for_gemm(((items_max + 7) / 8) * kUmmaBM, T, num_sms);
   UmmaParams p{};
   p.M = 0;
   p.K = g.K;
