@@ -319,43 +319,77 @@ def time_layer(bd, torch, layer, comm, ids, steps, warmup, use_graph, barrier):
         per.append(ms / steps * 1e3)
     return total, per, launches
 def time_e2e(bd, torch, layer, comm, ids_np, steps, warmup, barrier):
-    """Same step through the public API with HOST buffers: one pinned H2D copy of the step's inputs
-    (every projection's activations + the ids, packed), the four forwards, one D2H copy of the four
-    outputs -- all inside the timed region (graph-captured).  Returns (ms, h2d bytes, d2h bytes)."""
+    """Same step through the public API with HOST buffers: every step uploads its inputs (every
+    projection's activations + the ids, packed) from pinned host memory, runs the four forwards and
+    downloads the four outputs -- all inside the timed region (graph-captured).  As a server does, the
+    transfers run on a copy stream, double-buffered: step k+1's upload overlaps step k's forwards and step
+    k's download overlaps step k+1's.  Returns (ms, h2d bytes, d2h bytes) per the whole run."""
     dev = layer[0].X.device
     T = layer[0].X.shape[0]
     xs = [p.X.numel() for p in layer]
     ys = [p.Y.numel() for p in layer]
     nin = sum(xs) + 2 * T  # bf16 elements; ids (int32) packed as 2 bf16 slots each
-    h_in = torch.empty(nin, dtype=torch.bfloat16).pin_memory()
-    d_in = torch.empty(nin, dtype=torch.bfloat16, device=dev)
-    off = 0
-    dx = []
-    for p, n in zip(layer, xs):
-        h_in[off:off + n].copy_(p.X.reshape(-1).cpu())
-        dx.append(d_in[off:off + n].view(p.X.shape))
-        off += n
-    h_in[off:off + 2 * T].view(torch.int32).copy_(torch.from_numpy(ids_np.copy()))
-    did = d_in[off:off + 2 * T].view(torch.int32)
-    d_out = torch.empty(sum(ys), dtype=torch.bfloat16, device=dev)
-    h_out = torch.empty(sum(ys), dtype=torch.bfloat16).pin_memory()
-    dy = []
-    off = 0
-    for p, n in zip(layer, ys):
-        dy.append(d_out[off:off + n].view(p.Y.shape))
-        off += n
+    h_in = [torch.empty(nin, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    d_in = [torch.empty(nin, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    h_out = [torch.empty(sum(ys), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    d_out = [torch.empty(sum(ys), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    views = []
+    for b in range(2):
+        off, dx = 0, []
+        for p, n in zip(layer, xs):
+            h_in[b][off:off + n].copy_(p.X.reshape(-1).cpu())
+            dx.append(d_in[b][off:off + n].view(p.X.shape))
+            off += n
+        h_in[b][off:off + 2 * T].view(torch.int32).copy_(torch.from_numpy(ids_np.copy()))
+        did = d_in[b][off:off + 2 * T].view(torch.int32)
+        off, dy = 0, []
+        for p, n in zip(layer, ys):
+            dy.append(d_out[b][off:off + n].view(p.Y.shape))
+            off += n
+        views.append((dx, did, dy))
+    compute = torch.cuda.current_stream()
+    copy = torch.cuda.Stream()
+    ev = {name: [torch.cuda.Event() for _ in range(2)] for name in ("in_ready", "in_free", "out_ready", "out_free")}
 
-    def step(k):
-        d_in.copy_(h_in, non_blocking=True)
-        for p, x, y in zip(layer, dx, dy):
-            p.run(bd, comm, did, k, X=x, Y=y)
-        h_out.copy_(d_out, non_blocking=True)
+    def run(nsteps):
+        copy.wait_stream(compute)  # fork
+        for k in range(nsteps):
+            b = k % 2
+            dx, did, dy = views[b]
+            with torch.cuda.stream(copy):
+                if k >= 2:
+                    copy.wait_event(ev["in_free"][b])
+                d_in[b].copy_(h_in[b], non_blocking=True)
+                ev["in_ready"][b].record(copy)
+            compute.wait_event(ev["in_ready"][b])
+            if k >= 2:
+                compute.wait_event(ev["out_free"][b])
+            for p, x, y in zip(layer, dx, dy):
+                p.run(bd, comm, did, k, X=x, Y=y)
+            ev["in_free"][b].record(compute)
+            ev["out_ready"][b].record(compute)
+            with torch.cuda.stream(copy):
+                copy.wait_event(ev["out_ready"][b])
+                h_out[b].copy_(d_out[b], non_blocking=True)
+                ev["out_free"][b].record(copy)
+        compute.wait_stream(copy)  # join
 
-    for w in range(warmup):
-        step(w)
+    run(max(warmup, 2))
     torch.cuda.synchronize()
-    ms = graph_time(torch, step, steps, barrier)
-    return ms, nin * 2, sum(ys) * 2
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run(steps)
+    g.replay()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    start.record()
+    g.replay()
+    end.record()
+    torch.cuda.synchronize()
+    barrier()
+    return start.elapsed_time(end), nin * 2, sum(ys) * 2
 
 
 # ============================================================================ oracle legs
