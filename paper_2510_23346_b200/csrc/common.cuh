@@ -38,6 +38,17 @@ struct Geom {
   int C;                  // chunks of v read by the expand (S-LoRA column after all-gather: N)
 };
 
+// Profiling stamp inside lora_chunk16 (bdlora_debug_trace): %globaltimer into slot k of this CTA's trace row
+// when a trace row is passed; one predicated branch otherwise.
+#define LC_STAMP(k)                                                    \
+  do {                                                                 \
+    if (trace && etid == 0) {                                          \
+      long long t_;                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory"); \
+      trace[k] = t_;                                                   \
+    }                                                                  \
+  } while (0)
+
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float f[8]) {
   f[0] = __uint_as_float(u.x << 16);
   f[1] = __uint_as_float(u.x & 0xffff0000u);
@@ -171,30 +182,14 @@ __device__ __forceinline__ void lora_chunk16(float (&lr)[16], int n, int tb, int
   const bool staged = s_v != nullptr && g.C * 16 * per_tok <= s_v_cap;
   if (staged) {
     asm volatile("bar.sync 1, 128;" ::: "memory");  // previous readers of s_v are done
-    if (trace && etid == 0) {
-      long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[18] = t;
-    }
+    LC_STAMP(18);
     for (int c = 0; c < g.C; ++c) {
       const float* src = v + (size_t)(c * T + tb) * per_tok;
       float* dst = s_v + (size_t)c * 16 * per_tok;
       for (int idx = etid; idx < cnt * per_tok; idx += 128) dst[idx] = __ldg(src + idx);
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (trace && etid == 0) {
-      long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[19] = t;
-    }
-#define LC_STAMP(k)                                                    \
-  do {                                                                 \
-    if (trace && etid == 0) {                                          \
-      long long t_;                                                    \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory"); \
-      trace[k] = t_;                                                   \
-    }                                                                  \
-  } while (0)
+    LC_STAMP(19);
   }
   if (n >= g.M) return;
   LC_STAMP(20);
