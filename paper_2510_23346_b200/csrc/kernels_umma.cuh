@@ -198,18 +198,6 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
-    if constexpr (MODE == 0) {
-      // first ring of weight tiles straight away (weights never depend on the preceding kernel): the loads
-      // are in flight while TMEM is allocated and the CTA synchronises.  Expect only (no arrival): a stage
-      // cannot complete before the producer adds X (and A) after the programmatic-dependency wait.
-      const uint64_t pol_w = ptx::policy_evict_first();
-      const int P = min(u_hi - u_lo, p.nstages);
-      for (int idx = 0; idx < P; ++idx) {
-        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, mt = tile % M_TILES;
-        ptx::mbar_expect_tx(&full[idx], S::kWBytes);
-        ptx::tma_load_2d(sW + idx * S::kWBytes, &tmW, &full[idx], kb * kUmmaBK, mt * kUmmaBM, pol_w);
-      }
-    }
   }
   if (warp == 1) ptx::tmem_alloc<S::kTmemCols>(tmem_holder);
   ptx::tc_fence_before();
@@ -261,7 +249,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       const uint64_t pol_x = ptx::policy_evict_last();
       const int nu = u_hi - u_lo;
       const int NS = p.nstages;
-      const int P = min(nu, NS);  // the first ring's W tiles were issued during setup (above)
+      const int P = min(nu, NS);
+      for (int idx = 0; idx < P; ++idx) {  // expect (no arrival yet): the stage cannot complete before X/A
+        const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks, mt = tile % M_TILES;
+        ptx::mbar_expect_tx(&full[idx], S::kWBytes);
+        ptx::tma_load_2d(sW + idx * S::kWBytes, &tmW, &full[idx], kb * kUmmaBK, mt * kUmmaBM, pol_w);
+      }
       if (nu > 0) UMMA_TRACE(2);
       if (p.pdl) ptx::pdl_wait();
       // K-local LoRA: A rows (arena row index per slice) of the token tile's single adapter, loaded only when
