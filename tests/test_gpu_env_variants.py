@@ -12,8 +12,9 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SUBSET = ("column_bd_8b_qkv or row_bd_8b_down or decode_lora_schedules or integer_mode or multitenant "
-          "or prefill_token_tiles or nfs_row")
+# decode (fused, split-K/cluster, stream-K), T = 64 multi-adapter, prefill token tiles, exact integer mode
+SUBSET = ("decode_lora_schedules or integer_mode_bit_exact_decode or integer_mode_bit_exact_row or multitenant "
+          "or prefill_token_tiles or full_size_bench")
 
 VARIANTS = {
     "global_fixup": {"BDLORA_CLUSTER": "0"},
