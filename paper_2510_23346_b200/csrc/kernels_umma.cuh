@@ -135,7 +135,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   uint8_t* sW = smem;
   uint8_t* sX = smem + S::kStages * S::kWBytes;
   uint8_t* sA = sX + S::kStages * S::kXBytes;  // [kStages][16 x 64] adapter A rows (kHasA)
-  constexpr bool kA = S::kHasA && MODE == 0;
+  // MODE 0: base GEMM + LoRA expand (v from a preceding shrink, tensor-core expand for T > 16);
+  // MODE 2: the same GEMM as the single-kernel forward (grid-wide / K-local shrink inside) -- a separate
+  // instantiation so each path gets its own register allocation and executed footprint; MODE 1: shrink.
+  constexpr bool kGemm = MODE != 1;
+  constexpr bool kDec = MODE == 2;
+  constexpr bool kA = S::kHasA && kDec;
   uint64_t* full = (uint64_t*)(smem + S::kBarOff);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
           phase ^= 1;
         }
       }
-    } else if (MODE == 0 && ptx::elect_one()) {
+    } else if (kGemm && ptx::elect_one()) {
       const uint64_t pol_w = ptx::policy_evict_first();
       const uint64_t pol_x = ptx::policy_evict_last();
       const int nu = u_hi - u_lo;
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         // LoRA expand passes (every contributor of the tile takes its share, possibly one empty "last" pass):
         // issued as soon as the epilogue warps have built them, interleaved with the base k-blocks
         // (accumulation order is free in fp32), so the operand gathers overlap the weight stream
-        const bool lduty = (MODE == 0) && p.tcx;
+        const bool lduty = kGemm && !kDec && p.tcx;
         bool ldone = !lduty;
         auto lora_pass = [&]() {
           constexpr uint32_t kSbo = (S::kKp / 8) * 128;  // V: 8-row group stride
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..5)
-    if constexpr (MODE == 0) {
+    if constexpr (kGemm) {
     const int q = warp & 3;  // TMEM lane quarter accessible by this warp
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 64;  // 0..127
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     LoraPre pre;
     pre.a = -1;
     pre.sb = S::kHasA ? s_preb + etid : nullptr;  // decode: B rows live in shared memory, not registers
-    if (p.fuse && !local) {
+    if (kDec && p.fuse && !local) {
       // ---- fused shrink (matmul_3 / matmul_5): v[t][j][k] = s_a sum_d X[t][d] A_{a,j}[k][d] -----------
       // Units (leader token t, slice j, rank row k) are computed by the epilogue warps while the
       // producer/MMA warps stream W; a unit is computed once per DISTINCT adapter (leader = first token
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             }
         }
         s_lead[i] = lead;
-        if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups) + its slot metadata
+        if (!kDec && p.tcx) {  // leader within the whole token tile (tensor-core expand groups) + its slot metadata
           bool f = a >= 0;
           for (int i2 = 0; i2 < i && f; ++i2) f = (s_ids[i2] != a);
           s_mem[i] = f ? 1 : 0;
@@ -567,7 +572,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       if (!p.tcx) lora_pre16(pre, mt * kUmmaBM + row, min(16, tv), s_ids, s_lead, p.tab, p.arena, p.g);
 
     }
-    if (p.fuse && !local) {
+    if (kDec && p.fuse && !local) {
       // every unit of the launch published before any expand reads v
       if (etid == 0) {
         UMMA_TRACE(13);
@@ -608,7 +613,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
               }
           }
           s_lead[i] = lead;
-          if (p.tcx) {  // leader within the whole token tile (tensor-core expand groups) + its slot metadata
+          if (!kDec && p.tcx) {  // leader within the whole token tile (tensor-core expand groups) + its slot metadata
             bool f = a >= 0;
             for (int i2 = 0; i2 < i && f; ++i2) f = (s_ids[i2] != a);
             s_mem[i] = f ? 1 : 0;
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         ptx::named_bar_sync(1, 128);
         cur_nt = nt;
       }
-      if (p.tcx) {
+      if (!kDec && p.tcx) {
         // ---- tensor-core expand: this CTA's share of the tile's LoRA columns, built while weights stream ----
         // The tile's rank columns (leader i, slice j in [jlo, jhi], 8-row block) are numbered in (i, j, block)
         // order through a parallel prefix over the tile's adapter groups; passes of KC columns are dealt
@@ -1089,7 +1094,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
     }
   }
 
-  if (MODE == 0 && p.cluster > 1 && warp < 2) {  // the epilogue's cluster barriers count every thread
+  if (kGemm && p.cluster > 1 && warp < 2) {  // the epilogue's cluster barriers count every thread
     ptx::cluster_arrive();
     ptx::cluster_wait();
     if (kSlotsInRing) {
@@ -1253,7 +1258,7 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
   using S = UmmaSmem<BN>;
   UmmaParams p1 = p0;
   p1.nstages = std::min(S::kStages, umma_stage_cap(p0.T));
-  while (MODE == 0 && p1.cluster > 1) {
+  while (MODE != 1 && p1.cluster > 1) {
     // every cluster must be co-resident in one wave (one CTA per SM)
     static int max_clusters[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
     int& mc = max_clusters[p1.cluster];
@@ -1292,7 +1297,7 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
     p1.cluster -= 1;
     p1.grid = tiles * p1.cluster;
   }
-  if (MODE == 0 && p0.cluster > 1) {
+  if (MODE != 1 && p0.cluster > 1) {
     // the K-local LoRA adds a 2 KB A box to every k-block: worth it only where the tail dominates (cluster
     // reduce, short K segments -- measured alone: 8B O (16 k-blocks/CTA) -1.5 us but +1 us in the layer chain,
     // 8B down (56) +5 us); otherwise the grid-wide shrink hides under the stream
@@ -1315,7 +1320,7 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
   attr[0].val.programmaticStreamSerializationAllowed = p0.pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (MODE == 0 && p1.cluster > 1) {
+  if (MODE != 1 && p1.cluster > 1) {
     attr[1].id = cudaLaunchAttributeClusterDimension;
     attr[1].val.clusterDim.x = p1.cluster;
     attr[1].val.clusterDim.y = 1;
@@ -1402,8 +1407,8 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.fuse = v_fused ? 1 : 0;
   p.v_out = v_fused;
   p.rs_max = rs_max;
-  // decode-sized token tiles (BN = 16) expand on the CUDA cores; larger fused batches on the tensor cores
-  p.tcx = (!tensor_expand_enabled() || (v_fused && BN == 16)) ? 0 : tcx;
+  // the single-kernel forward (MODE 2 instantiation) expands on the CUDA cores; the rest on the tensor cores
+  p.tcx = (!tensor_expand_enabled() || v_fused) ? 0 : tcx;
   if (v_fused) p.v = v_fused;
   p.pdl = pdl;
   p.trace = g_umma_trace;
@@ -1417,7 +1422,8 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   if (!encode_kmajor(&tmW, W, p.K, p.M, kUmmaBM)) return 3;
   if (!encode_kmajor(&tmX, X, p.K, p.T, BN)) return 3;
   // without K-local LoRA the A boxes are dummies (row 0 of the arena map, or of X): same bytes, ignored
-  return umma_dispatch_bn<0>(BN, p, tmW, tmX, amap ? *amap : tmX, st);
+  return p.fuse ? umma_dispatch_bn<2>(BN, p, tmW, tmX, amap ? *amap : tmX, st)
+                : umma_dispatch_bn<0>(BN, p, tmW, tmX, amap ? *amap : tmX, st);
 }
 
 // Tensor-core shrink: v[t][j][k] = s_a X[t] . A_{a,j}[k] for every token t of every distinct adapter a,
