@@ -114,6 +114,16 @@ int bdlora_set_pdl(int enable);
    2 = same eligibility as 1 (kept for compatibility).  Results agree to fp32 summation order.
    Also settable with the environment variable BDLORA_LOCAL.  E_ARG for other values.                */
 int bdlora_set_decode_lora(int mode);
+/* Schedule knobs read once per process from the environment.  They change scheduling only, never values
+   (tests/test_gpu_env_variants.py re-runs the parity tests under each); the defaults are the measured best:
+     BDLORA_CLUSTER=0         split-K partials through global memory instead of a thread-block cluster
+     BDLORA_CLUSTER_SHRINK=0  keep the split when its clusters do not fit one wave (global fix-up)
+     BDLORA_STREAMK_CTAS=n    CTAs of a stream-K launch (default: whole tiles per CTA, else 0.86 x #SM)
+     BDLORA_FUSED_MAX_T=n     largest batch served by the single-kernel forward (default 16, max 256)
+     BDLORA_TC_EXPAND=0       LoRA expand on the CUDA cores for T > 16 too
+     BDLORA_LOCAL / BDLORA_LOCAL_MAXKB   see bdlora_set_decode_lora
+     BDLORA_STAGES=n          cap on the weight-ring depth;  BDLORA_GRID_CAP=n  cap on the SMs used
+     BDLORA_DEBUG=1           print the cluster / split decisions to stderr                            */
 /* Profiling hook: if non-NULL, subsequent tensor-core GEMM launches record per-CTA %globaltimer
    stamps (32 int64 per CTA) into this device buffer (>= 148*32*8 bytes); NULL turns it off.      */
 int bdlora_debug_trace(void* device_buffer);
