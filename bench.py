@@ -39,18 +39,36 @@ WORKLOADS = {
     # configs[1] -- the bench line
     "8b-decode-bs1-r16": dict(arch="llama-3.1-8b", T=1, ranks=[16], n_adapters=1, ids="single",
                               desc="configs[1]: Llama-3.1-8B layer shapes (h=4096, ff=14336, GQA 32/8), decode batch 1, rank 16"),
+    # configs[1] variants: 64 resident adapters with 1 active; the paper's parameter-matched pairing
+    # (BD 2r vs S-LoRA r, 0.86x the parameters)
+    "8b-decode-bs1-r16-64resident": dict(arch="llama-3.1-8b", T=1, ranks=[16], n_adapters=64, ids="single",
+                                         desc="configs[1] variant: 64 resident rank-16 adapters, 1 active, decode batch 1"),
+    "8b-decode-bs1-bd32-vs-slora16": dict(arch="llama-3.1-8b", T=1, ranks=[32], slora_ranks=[16], n_adapters=1,
+                                          ids="single",
+                                          desc="configs[1] parameter-matched pair: BD-LoRA rank 32 vs S-LoRA rank 16 "
+                                               "(P:801-805), decode batch 1"),
     # configs[3]
     "70b-decode-bs64-r32": dict(arch="llama-3.1-70b", T=64, ranks=[32], n_adapters=1, ids="single",
                                 desc="configs[3]: Llama-3.1-70B layer shapes, decode batch 64, rank 32"),
     "70b-decode-bs1-r32": dict(arch="llama-3.1-70b", T=1, ranks=[32], n_adapters=1, ids="single",
                                desc="configs[3]: Llama-3.1-70B layer shapes, decode batch 1, rank 32"),
-    # configs[4]
+    # configs[4] and its id-distribution variants (every request a different adapter)
     "70b-multitenant": dict(arch="llama-3.1-70b", T=64, ranks=[8, 16, 32, 64, 128], n_adapters=128, ids="uniform",
                             desc="configs[4]: 64 requests over 128 resident adapters (r in 8..128), Llama-3.1-70B shapes"),
-    # configs[2]
-    "8b-prefill-1024-r64": dict(arch="llama-3.1-8b", T=1024, ranks=[64], n_adapters=1, ids="single",
-                                desc="configs[2]: Llama-3.1-8B prefill 1024 tokens, rank 64, one segment"),
+    "70b-multitenant-zipf": dict(arch="llama-3.1-70b", T=64, ranks=[8, 16, 32, 64, 128], n_adapters=128, ids="zipf",
+                                 desc="configs[4] variant: Zipf(1.0) adapter popularity over 128 resident adapters"),
+    "70b-multitenant-distinct": dict(arch="llama-3.1-70b", T=64, ranks=[8, 16, 32, 64, 128], n_adapters=128,
+                                     ids="distinct",
+                                     desc="configs[4] variant: all 64 requests use different adapters (P:730-731)"),
 }
+# configs[2]: the rank sweep, one request (1 segment) and 8 requests x 128 tokens over 8 adapters (8 segments)
+for _r in (8, 32, 64, 128, 256):
+    WORKLOADS[f"8b-prefill-1024-r{_r}"] = dict(
+        arch="llama-3.1-8b", T=1024, ranks=[_r], n_adapters=1, ids="single",
+        desc=f"configs[2]: Llama-3.1-8B prefill 1024 tokens, rank {_r}, one segment")
+    WORKLOADS[f"8b-prefill-8x128-r{_r}"] = dict(
+        arch="llama-3.1-8b", T=1024, ranks=[_r], n_adapters=8, ids="segments", n_requests=8,
+        desc=f"configs[2]: Llama-3.1-8B prefill, 8 requests x 128 tokens over 8 rank-{_r} adapters (8 segments)")
 
 
 def log(*a):
@@ -146,10 +164,13 @@ def dist_env():
 # ============================================================================ layer construction
 
 class Projection:
-    """One adapted projection on one device: base weight replicas, pool(s), buffers."""
+    """One adapted projection on one device: base weight replicas, pool(s), buffers.
+
+    Weight replicas: at least `replicas` (the layer's count) and at least 3 x L2 of this projection's own
+    bytes, so the projection timed ALONE also streams its weights from HBM."""
 
     def __init__(self, bd, torch, proj, sharding, n, i, ranks_of_slots, scale_of_slots, T, dev, replicas, gen,
-                 w_replicas=None):
+                 w_replicas=None, keep_slots=()):
         self.proj, self.sharding, self.n, self.i = proj, sharding, n, i
         par = bd.COLUMN if proj.parallel == "column" else bd.ROW
         sh = {"bd": bd.SHARD_BD, "slora": bd.SHARD_SLORA, "nfs": bd.SHARD_NFS}[sharding]
@@ -157,6 +178,7 @@ class Projection:
         self.pool = bd.bdlora_create_pool(par, sh, n, i, proj.d_in, proj.d_out, cap, max(ranks_of_slots), device=dev.index)
         k, m = self.pool.k_loc, self.pool.m_loc
         self.k, self.m = k, m
+        self.kept = {}  # slot -> (rank, scale, A list, B list) in the load format (bench self-check)
         # adapters: factors generated in the load format on the device (synthetic, seeded), then sliced
         for a, (r, s) in enumerate(zip(ranks_of_slots, scale_of_slots)):
             A, B = [], []
@@ -170,10 +192,14 @@ class Projection:
                     A.append((torch.randn(proj.d_in, ra, generator=gen, device=dev) / math.sqrt(proj.d_in)).to(torch.bfloat16))
                     B.append((torch.randn(r, dj, generator=gen, device=dev) / (s * math.sqrt(r / n))).to(torch.bfloat16))
             bd.bdlora_load_adapter(self.pool, a, r, s, A, B)
+            if a in keep_slots:
+                self.kept[a] = (r, s, A, B)
             del A, B
+        pbytes = 2 * k * m
+        self.n_reps = max(replicas, math.ceil(3 * L2_BYTES / pbytes))
         if w_replicas is None:
             w_replicas = [(torch.randn(m, k, generator=gen, device=dev) / math.sqrt(proj.d_in)).to(torch.bfloat16)
-                          for _ in range(replicas)]
+                          for _ in range(self.n_reps)]
         self.W = w_replicas
         self.X = (torch.randn(T, k, generator=gen, device=dev)).to(torch.bfloat16)
         self.Y = torch.empty(T, m, dtype=torch.bfloat16, device=dev)
@@ -213,22 +239,28 @@ def make_ids(torch, wl, T, seed, dev):
         ids = np.zeros(T, np.int32)
     elif wl["ids"] == "uniform":
         ids = synth.ids_uniform(rng, T, wl["n_adapters"])
+    elif wl["ids"] == "zipf":
+        ids = synth.ids_zipf(rng, T, wl["n_adapters"])
+    elif wl["ids"] == "distinct":
+        ids = synth.ids_distinct(rng, T, wl["n_adapters"])
+    elif wl["ids"] == "segments":
+        ids = synth.ids_segments(T, wl["n_requests"])
     else:
         raise ValueError(wl["ids"])
     return torch.from_numpy(ids).to(dev), ids
 
 
-def slot_ranks(wl):
-    ranks = wl["ranks"]
+def slot_ranks(wl, sharding="bd"):
+    ranks = wl.get("slora_ranks", wl["ranks"]) if sharding == "slora" else wl["ranks"]
     return [ranks[k % len(ranks)] for k in range(wl["n_adapters"])]
 
 
-def build_layer(bd, torch, wl, sharding, n, i, dev, seed=0, replicas=None, share_w=None):
+def build_layer(bd, torch, wl, sharding, n, i, dev, seed=0, replicas=None, share_w=None, keep_slots=()):
     import synth
 
     projs = synth.arch_projections(wl["arch"])
     T = wl["T"]
-    ranks = slot_ranks(wl)
+    ranks = slot_ranks(wl, sharding)
     scales = [synth.rs_scale(16.0, r, n, sharding) for r in ranks]
     from paper_2510_23346_b200 import accounting as acc
 
@@ -240,7 +272,8 @@ def build_layer(bd, torch, wl, sharding, n, i, dev, seed=0, replicas=None, share
     layer = []
     for k, p in enumerate(projs):
         wr = share_w[k].W if share_w is not None else None
-        layer.append(Projection(bd, torch, p, sharding, n, i, ranks, scales, T, dev, replicas, gen, w_replicas=wr))
+        layer.append(Projection(bd, torch, p, sharding, n, i, ranks, scales, T, dev, replicas, gen, w_replicas=wr,
+                                keep_slots=keep_slots))
     return layer, replicas
 
 
@@ -249,7 +282,7 @@ def algorithmic(wl, sharding, n, ids_np):
     import synth
     from paper_2510_23346_b200 import accounting as acc
 
-    ranks = slot_ranks(wl)
+    ranks = slot_ranks(wl, sharding)
     touched = sorted(set(int(a) for a in ids_np.tolist() if a >= 0))
     rt = [ranks[a] for a in touched]
     tok = [ranks[a] if a >= 0 else 0 for a in ids_np.tolist()]
@@ -347,11 +380,13 @@ def time_e2e(bd, torch, layer, comm, ids_np, steps, warmup, barrier):
             dy.append(d_out[b][off:off + n].view(p.Y.shape))
             off += n
         views.append((dx, did, dy))
-    compute = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
     ev = {name: [torch.cuda.Event() for _ in range(2)] for name in ("in_ready", "in_free", "out_ready", "out_free")}
 
     def run(nsteps):
+        # the stream current at CALL time: under torch.cuda.graph that is the capture stream, so the copy
+        # stream forks from it and joins back -- every H2D / D2H copy and event wait is captured in the graph
+        compute = torch.cuda.current_stream()
         copy.wait_stream(compute)  # fork
         for k in range(nsteps):
             b = k % 2
@@ -376,9 +411,11 @@ def time_e2e(bd, torch, layer, comm, ids_np, steps, warmup, barrier):
 
     run(max(warmup, 2))
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
+    g = torch.cuda.CUDAGraph(keep_graph=True)
     with torch.cuda.graph(g):
         run(steps)
+    census = graph_census(g)
+    g.instantiate()
     g.replay()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -389,7 +426,25 @@ def time_e2e(bd, torch, layer, comm, ids_np, steps, warmup, barrier):
     end.record()
     torch.cuda.synchronize()
     barrier()
-    return start.elapsed_time(end), nin * 2, sum(ys) * 2
+    return start.elapsed_time(end), nin * 2, sum(ys) * 2, census
+
+
+def graph_census(g):
+    """Node types of a captured CUDA graph (proves the e2e graph holds the per-step H2D/D2H copies)."""
+    try:
+        from cuda.bindings import runtime as rt
+
+        h = rt.cudaGraph_t(init_value=int(g.raw_cuda_graph()))
+        err, _, n = rt.cudaGraphGetNodes(h, 0)
+        err, nodes, n = rt.cudaGraphGetNodes(h, n)
+        out = {}
+        for nd in nodes[:n]:
+            e2, ty = rt.cudaGraphNodeGetType(nd)
+            name = str(ty).split(".")[-1].replace("cudaGraphNodeType", "").lower()
+            out[name] = out.get(name, 0) + 1
+        return out
+    except Exception as e:  # pragma: no cover
+        return {"error": repr(e)[:200]}
 
 
 # ============================================================================ oracle legs
@@ -421,6 +476,49 @@ def run_oracle_step(sample, ids):
             ol.column_layer(X, W, p.d_out, ads, ids, "bd", 1)
         else:
             ol.row_layer(X, W, ads, ids, "bd", 1)
+
+
+def oracle_check_bench_output(bd, torch, layer, ids, ids_np, n_samples=24, seed=0):
+    """Part of the cpu_baseline leg (the oracle runs only there): re-run each projection of the timed BD
+    layer once, eagerly, in the bench's own launch configuration (pools, T, workspace, replica 0), and
+    compare `n_samples` sampled outputs per projection with the fp64 oracle computed one by one
+    (oracle.lora_layer_sampled).  N = 1 only, where the device output is the unsharded layer and the
+    load format of every factor is its dense form.  Returns the worst errors seen."""
+    import numpy as np
+
+    from oracle import lora as ol
+
+    rng = np.random.default_rng(seed)
+    worst_rel, n_tot, ok = 0.0, 0, True
+    per = {}
+    for p in layer:
+        p.run(bd, None, ids, 0)
+        torch.cuda.synchronize()
+        T, M = p.Y.shape
+        X = p.X.float().cpu().numpy().astype(np.float64)
+        ts = rng.integers(0, T, size=n_samples)
+        cs = rng.integers(0, M, size=n_samples)
+        got = p.Y[torch.from_numpy(ts).to(p.Y.device), torch.from_numpy(cs).to(p.Y.device)].float().cpu().numpy()
+        ref = np.empty(n_samples)
+        col0 = np.cumsum([0] + list(p.proj.d_out))
+        for q, (t, c) in enumerate(zip(ts.tolist(), cs.tolist())):
+            j = int(np.searchsorted(col0, c, side="right") - 1)
+            wcol = p.W[0][c].float().cpu().numpy().astype(np.float64)[:, None]  # W[:, c] (paper orientation)
+            ads = {}
+            a = int(ids_np[t])
+            if a >= 0:
+                r, sc, A, B = p.kept[a]
+                Aj = A[j].float().cpu().numpy().astype(np.float64)
+                Bc = B[j][:, c - col0[j]].float().cpu().numpy().astype(np.float64)[:, None]
+                ads[a] = (sc, Aj, Bc)
+            ref[q] = ol.lora_layer_sampled(X, wcol, ads, ids_np, [(t, 0)])[0]
+        good, m, l1 = ol.within_tolerance(got, ref)
+        ok = ok and good
+        worst_rel = max(worst_rel, m)
+        n_tot += n_samples
+        per[p.proj.name] = {"max_rel": m, "l1_rel": l1, "ok": good}
+    return {"ok": ok, "samples": n_tot, "worst_max_rel": worst_rel, "per_projection": per,
+            "tolerance": "max|y-ref| <= 2e-2 max|ref|, sum|y-ref|/sum|ref| <= 5e-3 (SURVEY 8(c) step 7)"}
 
 
 def cores_used():
@@ -497,7 +595,8 @@ def run_ours(args, wl):
     hbm_peak, tf_peak, tf_sus, peak_src = measured_peaks()
 
     # ---------------- BD-LoRA layer (the step) ----------------
-    layer, reps = build_layer(bd, torch, wl, "bd", n, rank, dev)
+    keep = sorted(set(int(a) for a in ids_np.tolist() if a >= 0)) if world == 1 else ()
+    layer, reps = build_layer(bd, torch, wl, "bd", n, rank, dev, keep_slots=keep)
     clocks = ClockSampler(local)
     clocks.start()
     total_ms, per, launches = time_layer(bd, torch, layer, comm, ids, args.steps, args.warmup, not args.no_graph, barrier)
@@ -538,14 +637,23 @@ def run_ours(args, wl):
     layer_bytes = sum(b for b, _ in alg.values())
     layer_frac = layer_bytes / (ms_step * 1e-3) / 1e9 / hbm_peak
 
+    # ---------------- sampled oracle check of this run's own output (cpu_baseline leg, N = 1) ----------------
+    self_check = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        self_check = oracle_check_bench_output(bd, torch, layer, ids, ids_np)
+        if not self_check["ok"]:
+            log("bench self-check FAILED:", json.dumps(self_check))
+
     # ---------------- S-LoRA comparison (same box, same W) ----------------
     slora = None
     if not args.skip_slora:
         sl_layer, _ = build_layer(bd, torch, wl, "slora", n, rank, dev, share_w=layer)
         s_total, s_per, _ = time_layer(bd, torch, sl_layer, comm, ids, args.steps, args.warmup, not args.no_graph, barrier)
         s_total = reduce_max(s_total, dev)
+        s_bytes = sum(b for b, _ in algorithmic(wl, "slora", n, ids_np).values())
         slora = {"ms_per_step": s_total / args.steps, "tokens_per_s": T / (s_total / args.steps * 1e-3),
-                 "proj_us": dict(zip(names, s_per)),
+                 "proj_us": dict(zip(names, s_per)), "ranks": wl.get("slora_ranks", wl["ranks"]),
+                 "layer_hbm_frac": s_bytes / (s_total / args.steps * 1e-3) / 1e9 / hbm_peak,
                  "bd_speedup": (s_total / total_ms)}
         if comm is not None:
             slora["collectives"] = bd.bdlora_comm_stats(comm)
@@ -559,17 +667,21 @@ def run_ours(args, wl):
         nf_layer, _ = build_layer(bd, torch, wl, "nfs", n, rank, dev, share_w=layer)
         f_total, f_per, _ = time_layer(bd, torch, nf_layer, comm, ids, args.steps, args.warmup, not args.no_graph, barrier)
         f_total = reduce_max(f_total, dev)
+        f_bytes = sum(b for b, _ in algorithmic(wl, "nfs", n, ids_np).values())
         nfs = {"ms_per_step": f_total / args.steps, "tokens_per_s": T / (f_total / args.steps * 1e-3),
-               "proj_us": dict(zip(names, f_per)), "bd_speedup": (f_total / total_ms)}
+               "proj_us": dict(zip(names, f_per)),
+               "layer_hbm_frac": f_bytes / (f_total / args.steps * 1e-3) / 1e9 / hbm_peak,
+               "bd_speedup": (f_total / total_ms)}
         for p in nf_layer:
             p.close()
         del nf_layer
 
     # ---------------- e2e through the public API with host buffers ----------------
-    e2e_ms, h2d, d2h = time_e2e(bd, torch, layer, comm, ids_np, args.steps, args.warmup, barrier)
+    e2e_ms, h2d, d2h, census = time_e2e(bd, torch, layer, comm, ids_np, args.steps, args.warmup, barrier)
     e2e_ms = reduce_max(e2e_ms, dev)
     e2e = {"value": T / (e2e_ms / args.steps * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps}
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+           "graph_nodes": census, "graph_memcpy_nodes_expected": 2 * args.steps}
     collectives = bd.bdlora_comm_stats(comm) if comm is not None else None
     for p in layer:
         p.close()
@@ -608,7 +720,7 @@ def run_ours(args, wl):
                                              L, local_only=True) for tpn in (2, 4, 8)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.skip_cpu:
+    if rank == 0 and not args.skip_cpu:
         cpu = cpu_baseline(wl)
 
     if rank == 0:
@@ -624,7 +736,7 @@ def run_ours(args, wl):
             "layer_us": ms_step * 1e3, "proj_us": proj_us, "layer_hbm_frac": layer_frac,
             "layer_algorithmic_bytes": layer_bytes,
             "slora": slora, "nfs": nfs, "collectives": collectives, "tp_emulated_1gpu": tp_emulated,
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "decode_step": decode_step,
+            "roofline": roofline, "cpu_baseline": cpu, "self_check": self_check, "e2e": e2e, "decode_step": decode_step,
             "gpu_launches": launches * args.steps, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

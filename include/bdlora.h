@@ -159,7 +159,11 @@ int bdlora_destroy_pool(bdlora_pool* pool);
    the fp32 shrink output (e.g. alpha*sqrt(N)/sqrt(r) for BD; reading R1).  src_is_device:
    0 = host pointers (copied synchronously w.r.t. `stream`; sources may be freed on return),
    1 = device pointers (caller may free after `stream` completes).  Reloading a loaded slot
-   replaces it.                                                                                  */
+   replaces it; no forward that reads the slot may be in flight.  Ragged arena: the new copy is
+   allocated and staged before the old one is released, so a failed reload (E_CAPACITY, E_CUDA)
+   leaves the previous adapter loaded.  Fixed arena (arena_bytes = 0): the slot's own region is
+   rewritten, so a copy failure leaves the slot empty (E_NOT_LOADED on later use of the id is the
+   caller's contract, not checked on device).                                                    */
 int bdlora_load_adapter(bdlora_pool* pool, int32_t slot, int32_t rank, float scale,
                         const void* const* A, const void* const* B, int32_t src_is_device,
                         bdlora_stream_t stream);
@@ -183,8 +187,21 @@ int bdlora_pool_bytes(const bdlora_pool* pool, int64_t* resident, int64_t* arena
 int bdlora_pool_geometry(const bdlora_pool* pool, int32_t* k_loc, int32_t* m_loc);
 
 /* Workspace bytes needed by any forward of this pool for T tokens (device memory, caller-owned,
-   256-byte aligned base, reusable across calls on the same stream, contents undefined on entry). */
+   256-byte aligned base).  The first 64 KB are a COUNTER REGION at T-independent offsets (split-tile
+   arrival counters, the fused shrink's tickets): it must be ZERO before the workspace's first use
+   (bdlora_workspace_init, or any zero fill such as cudaMemset of the whole buffer) and every forward
+   leaves it zero again.  The rest is scratch, undefined on entry.  A workspace sized for T may then
+   serve any T' <= T of this pool, one call at a time in stream order (calls on different streams
+   need different workspaces).  An uninitialised counter region can make a forward spin or return a
+   wrong split-K sum -- it is not detected.                                                       */
 int bdlora_workspace_bytes(const bdlora_pool* pool, int64_t T, size_t* bytes);
+/* Zeroes the workspace's counter region on `stream` (E_ARG if ws_bytes < 64 KB).                 */
+int bdlora_workspace_init(const bdlora_pool* pool, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+/* Debug/test hook: the last tensor-core kernel launch made by the CALLING thread:
+   info[0] instantiation (0 GEMM + expand, 1 tensor-core shrink, 2 single-kernel decode forward,
+   3 lean decode forward), [1] token-tile width BN, [2] grid (CTAs), [3] cluster size, [4] ring stages,
+   [5] 128-row tiles, [6] token tiles, [7] 64-wide k-blocks.  info[0] = -1 before any launch.      */
+int bdlora_last_launch_info(int32_t info[8]);
 
 /* ---------------------------------------------------------------- routing metadata (a2) ----- */
 /* Segments = maximal runs of equal consecutive ids in token order (reading R10): writes

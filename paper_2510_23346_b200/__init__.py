@@ -28,7 +28,7 @@ __all__ = [
     "bdlora_load_adapter", "bdlora_unload_adapter", "bdlora_pool_bytes", "bdlora_pool_geometry",
     "bdlora_workspace_bytes", "bdlora_build_segments", "bdlora_column_forward", "bdlora_row_partial",
     "bdlora_row_forward", "slora_column_forward", "slora_row_forward", "bdlora_lora_shrink",
-    "bdlora_base_expand", "bdlora_v_elems", "make_workspace", "bdlora_set_decode_lora", "bdlora_load_adapter_blocks",
+    "bdlora_base_expand", "bdlora_v_elems", "make_workspace", "bdlora_workspace_init", "bdlora_last_launch_info", "bdlora_set_decode_lora", "bdlora_load_adapter_blocks",
 ]
 
 
@@ -261,10 +261,28 @@ def bdlora_v_elems(pool: Pool, T: int) -> int:
     return n.value
 
 
-def make_workspace(pool: Pool, T: int):
-    """Zero-filled device workspace (the library keeps its counter region zero between calls)."""
+def bdlora_workspace_init(pool: Pool, ws, stream=None) -> None:
+    """Zero the workspace's counter region (required once before first use; include/bdlora.h)."""
     torch = _torch()
-    return torch.zeros(bdlora_workspace_bytes(pool, T), dtype=torch.uint8, device=pool.tdevice)
+    _need(ws, "workspace", dtype=torch.uint8, device=pool.tdevice)
+    call("bdlora_workspace_init", pool.handle, _ptr(ws), ws.numel(), _stream(stream))
+
+
+def make_workspace(pool: Pool, T: int, stream=None):
+    """Device workspace for T tokens, counter region initialised (bdlora_workspace_init); the library
+    leaves the counters zero after every call."""
+    torch = _torch()
+    ws = torch.empty(bdlora_workspace_bytes(pool, T), dtype=torch.uint8, device=pool.tdevice)
+    bdlora_workspace_init(pool, ws, stream)
+    return ws
+
+
+def bdlora_last_launch_info() -> dict:
+    """The calling thread's last tensor-core kernel launch (include/bdlora.h): instantiation, BN, grid, ..."""
+    arr = (ctypes.c_int32 * 8)()
+    call("bdlora_last_launch_info", arr)
+    keys = ["kind", "bn", "grid", "cluster", "stages", "m_tiles", "n_tiles", "k_blocks"]
+    return dict(zip(keys, list(arr)))
 
 
 # ------------------------------------------------------------------------------------------ routing

@@ -31,7 +31,9 @@ namespace bdl {
 constexpr int kUmmaBM = 128;
 constexpr int kUmmaBK = 64;
 constexpr int kUmmaThreads = 192;
-constexpr int kFuseMaxT = 256;  // fused shrink / LoRA prefetch handle decode-sized batches (ids staged in smem)
+constexpr int kFuseMaxT = 256;
+constexpr int kUmmaMaxGrid = 1024;
+constexpr int kMaxDevices = 64;     // per-device caches of function attributes / occupancy answers  // bound of a splitting launch's grid (split-tile counters, workspace)  // fused shrink / LoRA prefetch handle decode-sized batches (ids staged in smem)
 
 struct UmmaParams {
   int M, K, T;
@@ -46,7 +48,7 @@ struct UmmaParams {
   const float* v;
   __nv_bfloat16* Y;
   float* part;    // [grid][2][128][BN] fp32 split-tile partials (slot 0: a CTA's first segment, 1: last)
-  int* tile_cnt;  // [m_tiles * n_tiles], zero between launches
+  int* tile_cnt;  // [kUmmaMaxGrid] split-tile arrival counters (by first contributor), zero between launches
   int pdl;
   int nstages;       // ring stages actually used (<= kStages): bounds the bytes in flight per SM
   int fuse;          // 1: the epilogue warps also compute v (fused shrink); 0: v comes from a prior kernel
@@ -971,8 +973,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         // barrier + cumulative fence order every thread's partial before it)
         ptx::named_bar_sync(1, 128);
         if (etid == 0) {
+          // counter of this split tile: indexed by its FIRST contributor (a CTA is the first contributor of at
+          // most one split tile -- its range would otherwise contain a whole tile in between), so the counter
+          // array is bounded by the grid, independent of T and M (fixed workspace offset)
           const int got = kb1 - kb0;
-          const int old = ptx::atom_add_acq_rel_gpu(p.tile_cnt + tile, got);
+          const int cf = umma_cta_of((long long)tile * p.k_blocks, UNITS, GRID);
+          const int old = ptx::atom_add_acq_rel_gpu(p.tile_cnt + cf, got);
           *s_last = (old + got == p.k_blocks);
         }
         ptx::named_bar_sync(1, 128);
@@ -1021,7 +1027,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
             }
           }
           if (etid == 0) {
-            p.tile_cnt[tile] = 0;
+            p.tile_cnt[c_first] = 0;
             UMMA_TRACE(10);
           }
         }
@@ -1120,6 +1126,8 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
 // Host side
 // ------------------------------------------------------------------------------------------------
 inline long long* g_umma_trace = nullptr;  // profiling hook (bdlora_debug_trace)
+// host-side record of this thread's last tensor-core kernel launch (bdlora_last_launch_info)
+inline thread_local int g_last_launch[8] = {-1, 0, 0, 0, 0, 0, 0, 0};
 
 // LoRA expand on the tensor cores (default) -- BDLORA_TC_EXPAND=0 selects the CUDA-core epilogue expand.
 inline bool tensor_expand_enabled() {
@@ -1197,14 +1205,14 @@ inline int umma_bn_for_gemm(int M, int T, int num_sms) {
   return best;
 }
 
-// Workspace: [sync: 3 ints, 256 B][tile counters][split-tile partials]
+// Counter region (fixed size, at a T-independent workspace offset, zero between launches):
+// [sync: 64 ints][split-tile counters: kUmmaMaxGrid ints]
+constexpr size_t kUmmaCounterBytes = 256 + kUmmaMaxGrid * sizeof(int);
+// Scratch (T-dependent): split-tile partials [grid][2][128][BN] fp32
 inline size_t umma_workspace_bytes(int M, int T, int num_sms = 148) {
+  (void)M;
   const int BN = umma_bn_for(T);  // the widest tile umma_bn_for_gemm may pick (partials)
-  const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM;
-  const int n_tiles = (T + std::min(BN, 64) - 1) / std::min(BN, 64);  // the most tiles it may pick (counters)
-  size_t part = (size_t)num_sms * 2 * BN * kUmmaBM * sizeof(float);
-  size_t cnt = (size_t)m_tiles * n_tiles * sizeof(int);
-  return 256 + ((cnt + 255) / 256) * 256 + part;
+  return (size_t)std::min(num_sms, kUmmaMaxGrid) * 2 * BN * kUmmaBM * sizeof(float);
 }
 
 inline bool umma_eligible(const Geom& g, int T) { return T >= 1 && g.K % kUmmaBK == 0 && g.K >= kUmmaBK; }
@@ -1258,10 +1266,20 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
   using S = UmmaSmem<BN>;
   UmmaParams p1 = p0;
   p1.nstages = std::min(S::kStages, umma_stage_cap(p0.T));
+  // function attributes and occupancy answers are per device context: cached per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = std::min(std::max(dev, 0), kMaxDevices - 1);
   while (MODE != 1 && p1.cluster > 1) {
     // every cluster must be co-resident in one wave (one CTA per SM)
-    static int max_clusters[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
-    int& mc = max_clusters[p1.cluster];
+    static int max_clusters[kMaxDevices][9];
+    static bool mc_init = false;
+    if (!mc_init) {
+      for (int d = 0; d < kMaxDevices; ++d)
+        for (int c = 0; c < 9; ++c) max_clusters[d][c] = -1;
+      mc_init = true;
+    }
+    int& mc = max_clusters[dev][p1.cluster];
     if (mc < 0) {
       if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                S::kBytes) != cudaSuccess)
@@ -1303,13 +1321,22 @@ inline int umma_launch_bn(const UmmaParams& p0, const CUtensorMap& tmW, const CU
     // 8B down (56) +5 us); otherwise the grid-wide shrink hides under the stream
     if (p1.cluster == 1 || p1.k_blocks / p1.cluster > local_max_kb()) p1.local = 0;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  if (!attr_set[dev]) {
     if (cudaFuncSetAttribute(umma_lora_gemm_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              S::kBytes) != cudaSuccess)
       return 2;
-    attr_set = true;
+    attr_set[dev] = true;
   }
+  // launch record (bdlora_last_launch_info): which instantiation and schedule this call took
+  g_last_launch[0] = MODE;
+  g_last_launch[1] = BN;
+  g_last_launch[2] = p1.grid;
+  g_last_launch[3] = (MODE != 1 && p1.cluster > 1) ? p1.cluster : 1;
+  g_last_launch[4] = p1.nstages;
+  g_last_launch[5] = p1.m_tiles;
+  g_last_launch[6] = p1.n_tiles;
+  g_last_launch[7] = p1.k_blocks;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p1.grid);
   cfg.blockDim = dim3(kUmmaThreads);
@@ -1345,8 +1372,8 @@ inline int umma_dispatch_bn(int BN, const UmmaParams& p, const CUtensorMap& tmW,
 
 // Returns 0 on launch, non-zero if the shape is not handled here.
 inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_bfloat16* W, const int* ids,
-                       const SlotEntry* tab, const __nv_bfloat16* arena, const float* v, __nv_bfloat16* Y, void* ws,
-                       int num_sms, cudaStream_t st, int pdl = 0, float* v_fused = nullptr, int rs_max = 0,
+                       const SlotEntry* tab, const __nv_bfloat16* arena, const float* v, __nv_bfloat16* Y, void* cnt,
+                       void* ws, int num_sms, cudaStream_t st, int pdl = 0, float* v_fused = nullptr, int rs_max = 0,
                        int tcx = 0, const CUtensorMap* amap = nullptr) {
   if (!umma_eligible(g, T)) return 1;
   if (v_fused && T > kFuseMaxT) return 1;
@@ -1399,10 +1426,10 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.g = g;
   p.v = v;
   p.Y = Y;
-  const size_t cnt_bytes = (((size_t)p.m_tiles * p.n_tiles * sizeof(int)) + 255) / 256 * 256;
-  p.sync = (int*)ws;
-  p.tile_cnt = (int*)((char*)ws + 256);
-  p.part = (float*)((char*)ws + 256 + cnt_bytes);
+  if (p.grid > kUmmaMaxGrid && !(BN >= 128 && tiles > num_sms)) return 1;  // split-tile counters bounded
+  p.sync = (int*)cnt;
+  p.tile_cnt = (int*)((char*)cnt + 256);
+  p.part = (float*)ws;
   p.X = X;
   p.fuse = v_fused ? 1 : 0;
   p.v_out = v_fused;
@@ -1430,7 +1457,7 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
 // the A rows gathered in 16-row TMA boxes through `amap` (the pool arena viewed as [rows, K]).  The item
 // list comes from route_kernel (launched just before).  Workspace as umma_workspace_bytes(items_max*16, T).
 inline size_t umma_shrink_workspace_bytes(int items_max, int T, int num_sms = 148) {
-  return umma_workspace_bytes(((items_max + 7) / 8) * kUmmaBM, T, num_sms);
+  return kUmmaCounterBytes;  // the shrink writes v directly (no partials); counters kept for uniformity
 }
 
 inline int umma_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* ids, const SlotEntry* tab,
@@ -1456,10 +1483,9 @@ inline int umma_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, cons
   p.g = g;
   p.v = nullptr;
   p.Y = nullptr;
-  const size_t cnt_bytes = (((size_t)p.m_tiles * p.n_tiles * sizeof(int)) + 255) / 256 * 256;
   p.sync = (int*)ws;
   p.tile_cnt = (int*)((char*)ws + 256);
-  p.part = (float*)((char*)ws + 256 + cnt_bytes);
+  p.part = nullptr;
   p.X = X;
   p.fuse = 0;
   p.tcx = 0;

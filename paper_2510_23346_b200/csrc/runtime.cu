@@ -132,13 +132,21 @@ int64_t slot_elems_for_rank(const bdlora_pool* p, int r) {
   return (e + K - 1) / K * K;
 }
 
-// Workspace layout (bytes, 256-aligned sections):
-//   [counters: int32 x kMaxTiles][v: C_w x T x J x Rc fp32][part: S*T x M fp32 (split-K partials)]
+// Workspace layout (bytes, 256-aligned sections).  The COUNTER REGION comes first, at offsets that depend
+// on nothing but constants: every counter is zero between calls (the kernels re-arm what they use), so a
+// workspace zero-filled once (bdlora_workspace_init) can serve any T' <= the T it was sized for.
+//   [gemv tile counters: int32 x kMaxTiles][tensor-core GEMM counters][shrink counters][spare]  (kCounterBytes)
+//   [v: C_w x T x J x Rc fp32][part: S*T x M fp32 (GEMV split-K)][GEMM partials][route][gather staging]
 constexpr int kMaxTiles = 8192;
 constexpr int kPartTokenSplits = 64;  // S x min(T, 8) <= 64 for the split-K GEMV
+constexpr size_t kOffUmmaCnt = sizeof(int) * kMaxTiles;                      // 32 KB
+constexpr size_t kOffShrinkCnt = kOffUmmaCnt + 8192;                           // tensor-core GEMM: sync + 1024 counters
+constexpr size_t kOffSpareCnt = kOffShrinkCnt + 8192;
+constexpr size_t kCounterBytes = kOffSpareCnt + 16384;                        // 64 KB
+static_assert(bdl::kUmmaCounterBytes <= 8192, "GEMM counter region");
 
 struct WsLayout {
-  size_t off_counters, off_v, off_part, off_umma, off_route, off_shrink, off_gather, total;
+  size_t off_counters, off_umma_cnt, off_shrink_cnt, off_v, off_part, off_umma, off_route, off_gather, total;
 };
 
 constexpr int kTcShrinkMinT = 17;  // phases API: tensor-core shrink above decode sizes
@@ -169,9 +177,10 @@ int fused_max_t() {
 
 WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   WsLayout L;
-  size_t o = 0;
-  L.off_counters = o;
-  o = align_up(o + sizeof(int) * kMaxTiles, 256);
+  L.off_counters = 0;
+  L.off_umma_cnt = kOffUmmaCnt;
+  L.off_shrink_cnt = kOffShrinkCnt;
+  size_t o = kCounterBytes;
   L.off_v = o;
   const int Cw = (p->d.sharding == BDLORA_SHARD_SLORA && p->d.parallel == BDLORA_COLUMN) ? p->d.tp_size : 1;
   o = align_up(o + sizeof(float) * (size_t)Cw * T * p->g.J * p->g.Rc, 256);
@@ -180,10 +189,8 @@ WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   L.off_umma = o;
   o = align_up(o + bdl::umma_workspace_bytes(p->g.M, (int)T, p->num_sms), 256);
   L.off_route = o;
-  const int items = tc_items_max(p, T);
+  const int items = tc_items_max(p, std::min<int64_t>(T, bdl::kRouteMaxSeg));
   if (items > 0) o = align_up(o + sizeof(int) * bdl::RouteLayout::kWords, 256);
-  L.off_shrink = o;
-  if (items > 0) o = align_up(o + bdl::umma_shrink_workspace_bytes(items, (int)T, p->num_sms), 256);
   L.off_gather = o;  // Alg. 2 all-gather staging: [N][T][M_loc] bf16 (column pools, N > 1)
   if (p->d.parallel == BDLORA_COLUMN && p->d.tp_size > 1) o = align_up(o + (size_t)p->d.tp_size * T * p->g.M * 2, 256);
   L.total = o;
@@ -216,48 +223,58 @@ int g_pdl = 1;  // programmatic dependent launch chaining (bdlora_set_pdl)
 
 WsLayout ws_layout(const bdlora_pool* p, int64_t T);
 
+// v = s X A[a] for T tokens.  Batches are processed in chunks of at most kRouteMaxSeg tokens (the route
+// kernel stages one chunk's segments in shared memory; shrink_rows_kernel stages one chunk's member list),
+// so any T the ABI accepts is served in O(T) work: chunk c covers tokens [c0, c0 + Tc) and writes v rows
+// [c0, c0 + Tc) (v is token-major inside each of its C chunks).
 int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids, float* v, cudaStream_t st,
                   void* ws = nullptr) {
   if (T == 0) return BDLORA_OK;
-  const int items = ws ? tc_items_max(p, T) : 0;
-  if (items > 0) {
-    // tensor-core shrink: route (groups + A boxes) -> grouped tcgen05 GEMM writing v
-    const WsLayout L = ws_layout(p, T);
-    int* route = (int*)((char*)ws + L.off_route);
+  const Geom& g = p->g;
+  const size_t per_tok = (size_t)g.J * g.Rc;
+  for (int c0 = 0; c0 < T; c0 += bdl::kRouteMaxSeg) {
+    const int Tc = std::min(T - c0, bdl::kRouteMaxSeg);
+    const void* Xc = (const char*)X + (size_t)c0 * g.K * 2;
+    const int32_t* idc = ids + c0;
+    float* vc = v + (size_t)c0 * per_tok;
+    const int items = ws ? tc_items_max(p, Tc) : 0;
+    if (items > 0) {
+      // tensor-core shrink: route (groups + A boxes) -> grouped tcgen05 GEMM writing v
+      const WsLayout L = ws_layout(p, T);
+      int* route = (int*)((char*)ws + L.off_route);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(1);
+      cfg.blockDim = dim3(1024);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CU_TRY(cudaLaunchKernelEx(&cfg, bdl::route_kernel, idc, Tc, (const SlotEntry*)p->d_tab, p->g, route, vc,
+                                (int)(Tc * per_tok)));
+      count_launch();
+      int rc = bdl::umma_shrink_launch(p->g, (const __nv_bfloat16*)Xc, Tc, idc, p->d_tab, route, p->amap, vc, items,
+                                       (char*)ws + L.off_shrink_cnt, p->num_sms, st, g_pdl);
+      if (rc != 0) return fail(BDLORA_E_CUDA, "tensor-core shrink launch failed (%d): %s", rc,
+                               cudaGetErrorString(cudaGetLastError()));
+      count_launch();
+      continue;
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1);
-    cfg.blockDim = dim3(1024);
+    cfg.gridDim = dim3(Tc, g.J, p->rs_max);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = sizeof(int) * (size_t)Tc;  // <= 16 KB
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CU_TRY(cudaLaunchKernelEx(&cfg, bdl::route_kernel, ids, T, (const SlotEntry*)p->d_tab, p->g, route, v,
-                              (int)(T * p->g.J * p->g.Rc)));
+    CU_TRY(cudaLaunchKernelEx(&cfg, bdl::shrink_rows_kernel<4>, (const __nv_bfloat16*)Xc, Tc, idc,
+                              (const SlotEntry*)p->d_tab, (const __nv_bfloat16*)p->arena, g, vc));
     count_launch();
-    int rc = bdl::umma_shrink_launch(p->g, (const __nv_bfloat16*)X, T, ids, p->d_tab, route, p->amap, v, items,
-                                     (char*)ws + L.off_shrink, p->num_sms, st, g_pdl);
-    if (rc != 0) return fail(BDLORA_E_CUDA, "tensor-core shrink launch failed (%d): %s", rc,
-                             cudaGetErrorString(cudaGetLastError()));
-    count_launch();
-    return BDLORA_OK;
   }
-  const Geom& g = p->g;
-  if (T > 65535 * 16) return fail(BDLORA_E_CAPACITY, "T = %d too large for the shrink grid", T);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(T, g.J, p->rs_max);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = sizeof(int) * (size_t)T;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CU_TRY(cudaLaunchKernelEx(&cfg, bdl::shrink_rows_kernel<4>, (const __nv_bfloat16*)X, T, ids,
-                            (const SlotEntry*)p->d_tab, (const __nv_bfloat16*)p->arena, g, v));
-  count_launch();
   return BDLORA_OK;
 }
 
@@ -308,8 +325,8 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
   if (bdl::umma_eligible(p->g, T)) {
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, T, (const __nv_bfloat16*)W, ids, p->d_tab,
-                              (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
-                              p->num_sms, st, pdl, nullptr, 0, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
+                              (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma_cnt,
+                              (char*)ws + L.off_umma, p->num_sms, st, pdl, nullptr, 0, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
     if (rc == 0) {
       count_launch();
       CU_TRY(cudaGetLastError());
@@ -648,14 +665,24 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
   DeviceGuard dg(p->dev);
   cudaStream_t st = (cudaStream_t)stream;
 
-  // release the previous occupant
-  if (p->h_tab[slot].loaded) bdlora_unload_adapter(p, slot);
+  // a reload keeps the previous occupant until the new one is staged: in the ragged arena the new region is
+  // allocated first (an allocation failure leaves the old adapter loaded and intact) and the old region is
+  // released only after the new table entry is in place; the fixed arena reuses the slot's own region, so
+  // a failure while copying leaves the slot empty
+  const bool reload = p->h_tab[slot].loaded != 0;
+  const SlotEntry old_e = p->h_tab[slot];
+  const int64_t old_elems = p->slot_elems[slot];
 
   int rs, re;
   ranks_for(p, rank, &rs, &re);
   const int64_t elems = slot_elems_for_rank(p, rank);
   int64_t off = 0;
   ST_TRY(arena_alloc(p, slot, elems, &off));
+  auto retire_old = [&]() {
+    if (!reload) return;
+    p->resident_elems -= old_elems;
+    arena_free(p, old_e.offA[0], old_elems);
+  };
 
   // full source shapes (paper orientation) per mode
   SlotEntry e{};
@@ -779,9 +806,17 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
   if (rc != BDLORA_OK) {
     cudaStreamSynchronize(st);
     cleanup();
-    arena_free(p, off, elems);
+    if (p->ragged) {
+      arena_free(p, off, elems);  // the previous occupant (if any) is untouched
+    } else if (reload) {          // fixed arena: the slot's region was partly overwritten
+      p->h_tab[slot] = SlotEntry{};
+      p->slot_elems[slot] = 0;
+      p->resident_elems -= old_elems;
+      cudaMemcpy(p->d_tab + slot, &p->h_tab[slot], sizeof(SlotEntry), cudaMemcpyHostToDevice);
+    }
     return rc;
   }
+  retire_old();
   p->h_tab[slot] = e;
   p->slot_elems[slot] = elems;
   p->resident_elems += elems;
@@ -827,6 +862,22 @@ int bdlora_workspace_bytes(const bdlora_pool* p, int64_t T, size_t* bytes) {
   if (!bytes) return fail(BDLORA_E_ARG, "bytes is NULL");
   if (T < 0) return fail(BDLORA_E_ARG, "T < 0");
   *bytes = ws_layout(p, std::max<int64_t>(T, 1)).total;
+  return BDLORA_OK;
+}
+
+int bdlora_workspace_init(const bdlora_pool* p, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_pool(p));
+  if (!ws) return fail(BDLORA_E_ARG, "workspace is NULL");
+  if (ws_bytes < kCounterBytes)
+    return fail(BDLORA_E_ARG, "workspace too small: %zu < %zu bytes (counter region)", ws_bytes, kCounterBytes);
+  DeviceGuard dg(p->dev);
+  CU_TRY(cudaMemsetAsync(ws, 0, kCounterBytes, (cudaStream_t)stream));
+  return BDLORA_OK;
+}
+
+int bdlora_last_launch_info(int32_t info[8]) {
+  if (!info) return fail(BDLORA_E_ARG, "info is NULL");
+  for (int k = 0; k < 8; ++k) info[k] = bdl::g_last_launch[k];
   return BDLORA_OK;
 }
 
@@ -880,8 +931,8 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
     // adapter group, else in the epilogue warps) while the weights stream
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, (int)T, (const __nv_bfloat16*)W, ids, p->d_tab,
-                              (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma,
-                              p->num_sms, st, g_pdl, v, p->rs_max, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
+                              (const __nv_bfloat16*)p->arena, v, (__nv_bfloat16*)Y, (char*)ws + L.off_umma_cnt,
+                              (char*)ws + L.off_umma, p->num_sms, st, g_pdl, v, p->rs_max, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
     if (rc == 0) {
       count_launch();
       CU_TRY(cudaGetLastError());

@@ -349,6 +349,71 @@ def test_slora_dense_is_plain_lora():
         assert np.allclose(outs[j], ref, rtol=1e-12, atol=1e-12)
 
 
+def _bf_slora_col_shard_v(X, A, s, ids_t, n, i):
+    """Pure-Python matmul_3 on device i: v^i = s x_t A[:, i*r/N:(i+1)*r/N] -- its rank chunk."""
+    d_in, r = len(A), len(A[0])
+    rb = r // n
+    return [s * sum(X[ids_t][d] * A[d][i * rb + k] for d in range(d_in)) for k in range(rb)]
+
+
+def _bf_slora_row_shard_v(X, A, s, t, n, i):
+    """Pure-Python matmul_5 on device i: v^i = s x_t[rows i] A[rows i, :] -- a full-rank partial."""
+    d_in, r = len(A), len(A[0])
+    bi = d_in // n
+    return [s * sum(X[t][d] * A[d][k] for d in range(i * bi, (i + 1) * bi)) for k in range(r)]
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_slora_column_gathered_v_bruteforce(n):
+    """The S-LoRA column payload after the all-gather: the concatenation, in rank order,
+    of every device's matmul_3 rank chunk equals the oracle's s x_t A_j (full rank), exactly on integers."""
+    rng = np.random.default_rng(40 + n)
+    d_in, d_out, r = 8, (8, 4), 8
+    ads = {a: {"rank": r, "scale": (2.0, -0.5, 1.0)[a], "A": [_int_mat(rng, (d_in, r)) for _ in d_out],
+               "B": [_int_mat(rng, (r, dj)) for dj in d_out]} for a in range(3)}
+    X = _int_mat(rng, (5, d_in))
+    ids = np.array([2, 0, -1, 2, 1])
+    Xl = X.tolist()
+    for j in range(len(d_out)):
+        got = ol.slora_column_gathered_v(X, ads, ids, j)
+        assert sorted(got) == [0, 1, 3, 4]  # no entry for id -1
+        for t, vec in got.items():
+            a = int(ids[t])
+            ref = []
+            for i in range(n):
+                ref += _bf_slora_col_shard_v(Xl, ads[a]["A"][j].tolist(), ads[a]["scale"], t, n, i)
+            assert vec.tolist() == ref, (n, j, t)
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_slora_row_reduced_v_bruteforce(n):
+    """The S-LoRA row payload after the all-reduce: the sum over devices of the matmul_5
+    partials (row block i of x_t and of A) equals the oracle's s x_t A (full input, full rank), exactly."""
+    rng = np.random.default_rng(50 + n)
+    d_in, r = 8, 4
+    ads = {a: {"rank": r, "scale": (0.25, 3.0)[a], "A": [_int_mat(rng, (d_in, r))], "B": [_int_mat(rng, (r, 6))]}
+           for a in range(2)}
+    X = _int_mat(rng, (4, d_in))
+    ids = np.array([1, -1, 0, 1])
+    got = ol.slora_row_reduced_v(X, ads, ids)
+    assert sorted(got) == [0, 2, 3]
+    for t, vec in got.items():
+        a = int(ids[t])
+        ref = [0.0] * r
+        for i in range(n):
+            part = _bf_slora_row_shard_v(X.tolist(), ads[a]["A"][0].tolist(), ads[a]["scale"], t, n, i)
+            ref = [x + y for x, y in zip(ref, part)]
+        assert vec.tolist() == ref, (n, t)
+    # and the expand that follows reproduces the S-LoRA row layer (R12: v replicated, B column-sharded)
+    W = _int_mat(rng, (d_in, 6))
+    y = ol.row_layer(X, W, ads, ids, "slora", n)
+    for t in range(4):
+        ref = X[t] @ W
+        if ids[t] >= 0:
+            ref = ref + got[t] @ ads[int(ids[t])]["B"][0]
+        assert np.array_equal(y[t], ref)
+
+
 @pytest.mark.parametrize("which", ["A", "B"])
 def test_zero_adapter_is_base(which):
     """P5: a zero adapter leaves y = XW exactly (bitwise)."""
