@@ -30,7 +30,16 @@ def nccl_dir() -> str:
 
 
 def sources():
-    return [os.path.join(CSRC, "runtime.cu")]
+    """Translation units, built in parallel into objects under build/ and linked into one .so."""
+    return [os.path.join(CSRC, "runtime.cu"), os.path.join(CSRC, "decode.cu")]
+
+
+# private headers of each translation unit (a change rebuilds only the units that include them)
+_TU_DEPS = {
+    "runtime.cu": ["runtime.cu", "common.cuh", "ptx.cuh", "kernels_core.cuh", "kernels_umma.cuh", "kernels_route.cuh",
+                   "decode.h", "../../include/bdlora.h"],
+    "decode.cu": ["decode.cu", "decode.h", "kernels_decode.cuh", "common.cuh", "ptx.cuh"],
+}
 
 
 def deps():
@@ -49,26 +58,50 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in deps())
 
 
+def _obj(src: str) -> str:
+    return os.path.join(ROOT, "build", os.path.basename(src) + ".o")
+
+
+def _obj_stale(src: str) -> bool:
+    o = _obj(src)
+    if not os.path.exists(o):
+        return True
+    t = os.path.getmtime(o)
+    return any(os.path.getmtime(os.path.normpath(os.path.join(CSRC, d))) > t
+               for d in _TU_DEPS.get(os.path.basename(src), [os.path.basename(src)]))
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     nc = nccl_dir()
-    cmd = [
+    os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    common = [
         NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-        "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
+        "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
         "-Xptxas", "-v" if verbose else "-O3",
         "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nc, "include"),
         "-DBDLORA_BUILD",
-        *sources(),
-        "-L", os.path.join(nc, "lib"), "-l:libnccl.so.2",
-        "-Xlinker", f"-rpath={os.path.join(nc, 'lib')}",
-        "-o", LIB + ".tmp",
     ]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    procs = []
+    for src in sources():
+        if force or _obj_stale(src):
+            cmd = common + ["-c", src, "-o", _obj(src) + ".tmp"]
+            procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    for src, cmd, pr in procs:
+        out, _ = pr.communicate()
+        if pr.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out)
+        if verbose:
+            sys.stderr.write(out)
+        os.replace(_obj(src) + ".tmp", _obj(src))
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+            *[_obj(s) for s in sources()],
+            "-L", os.path.join(nc, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", f"-rpath={os.path.join(nc, 'lib')}", "-o", LIB + ".tmp"]
+    r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if verbose:
-        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("link failed:\n" + " ".join(link) + "\n" + r.stdout + r.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

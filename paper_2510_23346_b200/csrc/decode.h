@@ -1,0 +1,41 @@
+// decode.h -- host interface of the lean decode kernel (kernels_decode.cuh), compiled in its own
+// translation unit (decode.cu) and called by runtime.cu.  C++ linkage, library-internal.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "common.cuh"
+
+namespace bdl {
+
+struct DecLaunch {
+  Geom g;
+  const __nv_bfloat16* X;
+  int T;                      // 1..16
+  const __nv_bfloat16* W;     // W^T [M, K] bf16, K-major
+  const int* ids;
+  const SlotEntry* tab;
+  const __nv_bfloat16* arena;
+  const float* v;             // lora == 2: v [C][T][J][Rc] fp32
+  __nv_bfloat16* Y;
+  void* cnt;                  // >= dec_counter_bytes() of zeroed counters (workspace counter region)
+  void* scratch;              // >= dec_scratch_bytes(num_sms) bytes
+  int num_sms;
+  cudaStream_t stream;
+  int pdl;
+  int lora;                   // 1 K-local, 2 v precomputed
+};
+
+constexpr int kDecMaxT = 16;
+constexpr int kDecLoraRowsHost = 32;  // == kDecLoraRows: K-local capacity (sum of the batch's distinct local ranks)
+
+size_t dec_counter_bytes();
+size_t dec_scratch_bytes(int num_sms);
+bool dec_eligible(const Geom& g, int T);
+bool dec_enabled();                        // BDLORA_DECODE=0 selects the older single-kernel forward
+// Returns 0 on launch, non-zero if the shape is not handled (caller falls back), negative on a CUDA error.
+int dec_launch(const DecLaunch& a);
+void dec_last_launch(int info[8]);
+void dec_set_trace(long long* buf);
+
+}  // namespace bdl

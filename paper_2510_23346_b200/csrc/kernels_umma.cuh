@@ -211,6 +211,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // Cluster split-K with dedicated partial slots: a CTA pushes into a peer's shared memory, which is only
+  // legal once the peer has started -- every thread arrives on the cluster barrier now and waits before its
+  // first DSMEM access (the ring-slot variant gets this from its post-mainloop cluster barrier).
+  const bool early_cl = kGemm && !kSlotsInRing && p.cluster > 1;
+  bool cl_pending = early_cl;
+  if (early_cl) ptx::cluster_arrive_relaxed();
   if (threadIdx.x == 0) {
     UMMA_TRACE(1);
     // dependents (the next kernel) may launch now: they wait for this grid's completion before
@@ -834,6 +840,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
         if (u == u_lo) UMMA_TRACE(5);
         UMMA_TRACE(6);
       }
+      if (cl_pending && !whole) {  // peers have started: DSMEM pushes below are legal
+        ptx::cluster_wait();
+        cl_pending = false;
+      }
       if (kSlotsInRing && !whole && p.cluster > 1) {
         // the partial slots live in the (then idle) weight rings: wait until every contributor of the
         // tile has finished its mainloop before anyone pushes
@@ -1038,6 +1048,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
       u += kb1 - kb0;
       if (etid == 0) UMMA_TRACE(7);
     }
+    if (cl_pending) ptx::cluster_wait();  // no split segment: still pair the early arrival
     } else {
       // ------------------------------------------------ shrink epilogue: v = s_a * acc, member tokens only
       const int q = warp & 3;
@@ -1101,6 +1112,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1)
   }
 
   if (kGemm && p.cluster > 1 && warp < 2) {  // the epilogue's cluster barriers count every thread
+    if (early_cl) ptx::cluster_wait();
     ptx::cluster_arrive();
     ptx::cluster_wait();
     if (kSlotsInRing) {

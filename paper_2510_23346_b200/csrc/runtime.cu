@@ -15,6 +15,7 @@
 
 #include "../../include/bdlora.h"
 #include "common.cuh"
+#include "decode.h"
 #include "kernels_core.cuh"
 #include "kernels_umma.cuh"
 
@@ -141,12 +142,14 @@ constexpr int kMaxTiles = 8192;
 constexpr int kPartTokenSplits = 64;  // S x min(T, 8) <= 64 for the split-K GEMV
 constexpr size_t kOffUmmaCnt = sizeof(int) * kMaxTiles;                      // 32 KB
 constexpr size_t kOffShrinkCnt = kOffUmmaCnt + 8192;                           // tensor-core GEMM: sync + 1024 counters
-constexpr size_t kOffSpareCnt = kOffShrinkCnt + 8192;
-constexpr size_t kCounterBytes = kOffSpareCnt + 16384;                        // 64 KB
+constexpr size_t kOffDecCnt = kOffShrinkCnt + 8192;                            // lean decode kernel: 1024 counters
+constexpr size_t kCounterBytes = kOffDecCnt + 16384;                          // 64 KB
 static_assert(bdl::kUmmaCounterBytes <= 8192, "GEMM counter region");
+thread_local int g_last_src = 0;  // bdlora_last_launch_info: 0 = tensor-core GEMM / shrink record, 1 = lean decode
 
 struct WsLayout {
-  size_t off_counters, off_umma_cnt, off_shrink_cnt, off_v, off_part, off_umma, off_route, off_gather, total;
+  size_t off_counters, off_umma_cnt, off_shrink_cnt, off_dec_cnt, off_v, off_part, off_umma, off_dec, off_route,
+      off_gather, total;
 };
 
 constexpr int kTcShrinkMinT = 17;  // phases API: tensor-core shrink above decode sizes
@@ -180,6 +183,7 @@ WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   L.off_counters = 0;
   L.off_umma_cnt = kOffUmmaCnt;
   L.off_shrink_cnt = kOffShrinkCnt;
+  L.off_dec_cnt = kOffDecCnt;
   size_t o = kCounterBytes;
   L.off_v = o;
   const int Cw = (p->d.sharding == BDLORA_SHARD_SLORA && p->d.parallel == BDLORA_COLUMN) ? p->d.tp_size : 1;
@@ -188,6 +192,8 @@ WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   o = align_up(o + sizeof(float) * (size_t)kPartTokenSplits * p->g.M, 256);
   L.off_umma = o;
   o = align_up(o + bdl::umma_workspace_bytes(p->g.M, (int)T, p->num_sms), 256);
+  L.off_dec = o;  // lean decode kernel: split-tile partials
+  if (T <= bdl::kDecMaxT) o = align_up(o + bdl::dec_scratch_bytes(p->num_sms), 256);
   L.off_route = o;
   const int items = tc_items_max(p, std::min<int64_t>(T, bdl::kRouteMaxSeg));
   if (items > 0) o = align_up(o + sizeof(int) * bdl::RouteLayout::kWords, 256);
@@ -259,6 +265,7 @@ int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids
       if (rc != 0) return fail(BDLORA_E_CUDA, "tensor-core shrink launch failed (%d): %s", rc,
                                cudaGetErrorString(cudaGetLastError()));
       count_launch();
+      g_last_src = 0;
       continue;
     }
     cudaLaunchConfig_t cfg = {};
@@ -318,10 +325,50 @@ int launch_gemv(const bdlora_pool* p, const void* X, int T, const void* W, const
   return BDLORA_OK;
 }
 
+// Lean decode kernel (kernels_decode.cuh) for T <= 16.  lora = 1: K-local shrink + expand inside the kernel;
+// 2: v precomputed (the expand of a forward whose collective sits between shrink and expand).
+int launch_decode(const bdlora_pool* p, const void* X, int T, const void* W, const int32_t* ids, const float* v,
+                  void* Y, void* ws, cudaStream_t st, int lora) {
+  const WsLayout L = ws_layout(p, T);
+  bdl::DecLaunch a;
+  a.g = p->g;
+  a.X = (const __nv_bfloat16*)X;
+  a.T = T;
+  a.W = (const __nv_bfloat16*)W;
+  a.ids = ids;
+  a.tab = p->d_tab;
+  a.arena = (const __nv_bfloat16*)p->arena;
+  a.v = v;
+  a.Y = (__nv_bfloat16*)Y;
+  a.cnt = (char*)ws + L.off_dec_cnt;
+  a.scratch = (char*)ws + L.off_dec;
+  a.num_sms = p->num_sms;
+  a.stream = st;
+  a.pdl = g_pdl;
+  a.lora = lora;
+  const int rc = bdl::dec_launch(a);
+  if (rc < 0) return fail(BDLORA_E_CUDA, "decode kernel launch: %s", cudaGetErrorString(cudaGetLastError()));
+  if (rc > 0) return -1;  // shape not handled here
+  count_launch();
+  g_last_src = 1;
+  return BDLORA_OK;
+}
+
+// K-local LoRA inside the decode kernel needs every adapter's shrink and expand device-local (BD / NFS, one v
+// chunk) and the batch's distinct adapters to fit the kernel's rank-row capacity in the worst case.
+bool decode_klocal_ok(const bdlora_pool* p, int T) {
+  if (p->d.sharding == BDLORA_SHARD_SLORA || p->g.C != 1) return false;
+  return (int64_t)std::min<int64_t>(T, p->d.capacity) * p->rs_max <= bdl::kDecLoraRowsHost;
+}
+
 int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W, const int32_t* ids, const float* v,
                        void* Y, void* ws, cudaStream_t st) {
   const int pdl = g_pdl;
   if (T == 0) return BDLORA_OK;
+  if (bdl::dec_enabled() && bdl::dec_eligible(p->g, T)) {
+    const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, 2);
+    if (rc >= 0) return rc;
+  }
   if (bdl::umma_eligible(p->g, T)) {
     const WsLayout L = ws_layout(p, T);
     int rc = bdl::umma_launch(p->g, (const __nv_bfloat16*)X, T, (const __nv_bfloat16*)W, ids, p->d_tab,
@@ -329,6 +376,7 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
                               (char*)ws + L.off_umma, p->num_sms, st, pdl, nullptr, 0, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
     if (rc == 0) {
       count_launch();
+      g_last_src = 0;
       CU_TRY(cudaGetLastError());
       return BDLORA_OK;
     }
@@ -377,6 +425,7 @@ int bdlora_set_decode_lora(int mode) {
 
 int bdlora_debug_trace(void* device_buffer) {
   bdl::g_umma_trace = (long long*)device_buffer;
+  bdl::dec_set_trace((long long*)device_buffer);
   return BDLORA_OK;
 }
 
@@ -877,7 +926,9 @@ int bdlora_workspace_init(const bdlora_pool* p, void* ws, size_t ws_bytes, bdlor
 
 int bdlora_last_launch_info(int32_t info[8]) {
   if (!info) return fail(BDLORA_E_ARG, "info is NULL");
-  for (int k = 0; k < 8; ++k) info[k] = bdl::g_last_launch[k];
+  int d[8];
+  bdl::dec_last_launch(d);
+  for (int k = 0; k < 8; ++k) info[k] = g_last_src == 1 ? d[k] : bdl::g_last_launch[k];
   return BDLORA_OK;
 }
 
@@ -926,6 +977,11 @@ int bdlora_base_expand(bdlora_pool* p, const void* X, int64_t T, const void* W, 
 static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y, void* ws,
                     cudaStream_t st) {
   float* v = ws_v(p, ws, T);
+  if (bdl::dec_enabled() && bdl::dec_eligible(p->g, (int)T) && decode_klocal_ok(p, (int)T)) {
+    // decode: ONE lean kernel -- base GEMM on the tensor cores, K-local LoRA shrink + expand in its epilogue
+    const int rc = launch_decode(p, X, (int)T, W, ids, nullptr, Y, ws, st, 1);
+    if (rc >= 0) return rc;
+  }
   if (bdl::umma_eligible(p->g, (int)T) && T <= fused_max_t()) {
     // decode: ONE kernel -- the LoRA shrink runs inside it (K-local on the tensor cores for a single
     // adapter group, else in the epilogue warps) while the weights stream
@@ -935,6 +991,7 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
                               (char*)ws + L.off_umma, p->num_sms, st, g_pdl, v, p->rs_max, /*tcx=*/1, p->amap_ok ? &p->amap : nullptr);
     if (rc == 0) {
       count_launch();
+      g_last_src = 0;
       CU_TRY(cudaGetLastError());
       return BDLORA_OK;
     }

@@ -23,7 +23,27 @@ VARIANTS = {
     "fused_t64": {"BDLORA_FUSED_MAX_T": "64"},
     "cuda_core_expand": {"BDLORA_TC_EXPAND": "0"},
     "no_k_local": {"BDLORA_LOCAL": "0"},
+    "single_kernel_decode_forward": {"BDLORA_DECODE": "0"},  # the round-1 decode path instead of the lean kernel
 }
+
+# the lean decode kernel's own knobs (tests/test_gpu_decode.py)
+DEC_VARIANTS = {
+    "dec_streamk_all_sms": {"BDLORA_DEC_CTAS": "148"},
+    "dec_two_stages": {"BDLORA_DEC_STAGES": "2"},
+    "dec_min_4_kblocks": {"BDLORA_DEC_MINKB": "4"},
+    "dec_grid_37": {"BDLORA_DEC_CTAS": "37"},
+}
+
+
+@pytest.mark.parametrize("name", sorted(DEC_VARIANTS))
+def test_decode_kernel_under_schedule_variant(name):
+    env = dict(os.environ, **DEC_VARIANTS[name])
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_decode.py"), "-m", "gpu",
+                        "-x", "-q", "-p", "no:cacheprovider"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    tail = "\n".join((r.stdout + r.stderr).strip().splitlines()[-15:])
+    assert r.returncode == 0, f"{name} {DEC_VARIANTS[name]}:\n{tail}"
+    assert " passed" in tail, tail
 
 
 @pytest.mark.parametrize("name", sorted(VARIANTS))

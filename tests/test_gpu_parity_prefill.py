@@ -145,10 +145,10 @@ def test_prefill_row_tiles(dev, name, proj, n, r, ids_kind):
 
 
 def test_prefill_tp1_qkv_full(dev):
-    """TP = 1 QKV at S = 1024 (BN = 256 over 48 row tiles x 4 token tiles), r = 64, 8 segments."""
+    """TP = 1 QKV at S = 1024 (BN = 128: 48 row tiles x 8 token tiles = 384 whole tiles), r = 64, 8 segments."""
     ads, X, w_loc, ids, ref = _column_case(3200, QKV, 1, 0, 1024, 64, "8seg")
     y, info = _run_column(dev, QKV, 1, 0, 64, ads, X, w_loc, ids)
-    assert info["bn"] == 256, info
+    assert info["bn"] == 128, info
     _assert_tol(y, ref, "qkv tp1")
 
 
