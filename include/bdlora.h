@@ -99,9 +99,12 @@ int bdlora_kernel_launches(int64_t* n);
 /* Programmatic dependent launch chaining (default ON): every kernel of a forward is launched with
    programmatic stream serialization and waits (griddepcontrol.wait) before reading anything the
    preceding kernel may have produced (X, ids, v) and before writing Y, so a forward's prologue and
-   weight stream overlap the tail of the preceding kernel.  Contract while ON: the base weight W and
-   the pool's adapter factors must not be written by the kernel immediately preceding a forward on
-   the same stream (they are streamed before the dependency resolves).  0 = plain stream order.   */
+   weight stream overlap the tail of the preceding kernel.  Contract while ON: the base weight W, the
+   pool's adapter factors and slot table, and the ids array must not be written by the KERNEL
+   immediately preceding a forward on the same stream (the decode kernel streams W and reads ids, the
+   slot entries and the adapters' B rows before the dependency resolves; X and v are read after it).
+   Copies, memsets and event waits before a forward are full dependencies and are always safe.
+   0 = plain stream order.                                                                         */
 int bdlora_set_pdl(int enable);
 /* Decode (T <= 16) LoRA schedule inside the fused single-kernel forward.  The layer is linear in a
    partition of K (y = sum_seg X_seg W_seg + s (X_seg A_seg) B, regrouping matmul_3/4 and matmul_5/6 of

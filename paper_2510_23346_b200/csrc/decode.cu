@@ -49,30 +49,81 @@ int env_int(const char* name, int dflt) {
   return s ? atoi(s) : dflt;
 }
 
-template <int S>
-int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, cudaStream_t st) {
-  using L = DecSmem<S>;
+template <int S, bool CL>
+int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
+                  cudaStream_t st) {
+  using L = DecSmem<S, CL>;
   static bool attr[kMaxDev] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   dev = std::min(std::max(dev, 0), kMaxDev - 1);
   if (!attr[dev]) {
-    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes) !=
+    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
         cudaSuccess)
+      return -1;
+    if (CL && cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                  cudaSuccess)
       return -1;
     attr[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.grid);
   cfg.blockDim = dim3(kDecThreads);
-  cfg.dynamicSmemBytes = L::kBytes;
+  // BDLORA_DEC_SMEM_PAD=1 (experiments): request enough shared memory that only one CTA fits per SM
+  static const int pad = env_int("BDLORA_DEC_SMEM_PAD", 0);
+  cfg.dynamicSmemBytes = pad ? 200 * 1024 : L::kBytes;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, dec_lora_gemm_kernel<S>, tmW, tmX, p) == cudaSuccess ? 0 : -1;
+  if (CL) {
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = p.cluster;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
+  }
+  return cudaLaunchKernelEx(&cfg, dec_lora_gemm_kernel<S, CL>, tmW, tmX, tmA, p) == cudaSuccess ? 0 : -1;
+}
+
+// Largest cluster size <= want (>= 2) with at least `need` co-resident clusters, cached per (device, size).
+int fit_cluster(int want, int need, int grid_per_cluster_tiles) {
+  static int cache[kMaxDev][kDecMaxCluster + 1];
+  static bool init = false;
+  if (!init) {
+    for (int d = 0; d < kMaxDev; ++d)
+      for (int c = 0; c <= kDecMaxCluster; ++c) cache[d][c] = -1;
+    init = true;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev = std::min(std::max(dev, 0), kMaxDev - 1);
+  for (int c = want; c >= 2; --c) {
+    int& mc = cache[dev][c];
+    if (mc < 0) {
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<4, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t qc = {};
+      qc.gridDim = dim3(c * grid_per_cluster_tiles);
+      qc.blockDim = dim3(kDecThreads);
+      qc.dynamicSmemBytes = DecSmem<4, true>::kBytes;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = c;
+      ca[0].val.clusterDim.y = 1;
+      ca[0].val.clusterDim.z = 1;
+      qc.attrs = ca;
+      qc.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<4, true>, &qc) != cudaSuccess) {
+        cudaGetLastError();
+        mc = 0;
+      }
+    }
+    if (mc >= need) return c;
+  }
+  return 1;
 }
 
 }  // namespace
@@ -110,8 +161,19 @@ int dec_launch(const DecLaunch& a) {
   const int tiles = p.m_tiles;
   long long grid;
   const int min_kb = std::max(1, env_int("BDLORA_DEC_MINKB", 1));
+  p.cluster = 1;
   if (tiles <= sms) {
-    const int s = std::max(1, std::min(sms / tiles, p.k_blocks / min_kb));
+    int s = std::max(1, std::min(sms / tiles, p.k_blocks / min_kb));
+    // the tile's s contributors reduce through a thread-block cluster (DSMEM) when s >= 2: the global
+    // last-arriver fix-up costs two dependent L2 round trips (atomic + partial loads, often cross-die)
+    static const int cl_max = std::min(kDecMaxCluster, env_int("BDLORA_DEC_CLUSTER", kDecMaxCluster));
+    if (s >= 2 && cl_max >= 2) {
+      const int c = fit_cluster(std::min(s, cl_max), 1, 1);
+      if (c >= 2) {
+        s = c;
+        p.cluster = c;
+      }
+    }
     grid = (long long)tiles * s;
   } else {
     grid = 0;
@@ -120,7 +182,10 @@ int dec_launch(const DecLaunch& a) {
     if (!grid) grid = sms;
   }
   const int override_ctas = env_int("BDLORA_DEC_CTAS", 0);
-  if (override_ctas > 0) grid = std::min<long long>(override_ctas, units);
+  if (override_ctas > 0) {
+    grid = std::min<long long>(override_ctas, units);
+    p.cluster = 1;
+  }
   grid = std::max<long long>(1, std::min<long long>(grid, units));
   if (grid > std::min(sms, kDecMaxGrid) && grid != tiles) grid = std::min(sms, kDecMaxGrid);
   p.grid = (int)grid;
@@ -139,17 +204,28 @@ int dec_launch(const DecLaunch& a) {
   CUtensorMap tmW, tmX;
   if (!encode(&tmW, a.W, p.K, p.M, kDecBM)) return 3;
   if (!encode(&tmX, a.X, p.K, p.T, kDecBN)) return 3;
-  const int stages = std::min(5, std::max(2, env_int("BDLORA_DEC_STAGES", 5)));
+  // Long weight streams (>= 16 k-blocks = 256 KB per CTA, e.g. TP1 / TP2 projections) take a deep 8-stage ring (one CTA
+  // per SM: the PDL overlap with the next projection matters little next to a 30+ us stream); the rest keep
+  // <= 113 KB so two CTAs share an SM across projection boundaries.
+  static const int deep_kb = env_int("BDLORA_DEC_DEEP_KB", 16);
+  const bool deep = deep_kb > 0 && units / p.grid >= deep_kb;
+  const int smax = deep ? 8 : p.cluster > 1 ? 4 : 5;
+  const int stages = std::min(smax, std::max(2, env_int("BDLORA_DEC_STAGES", smax)));
   p.nstages = stages;
   g_dec_last[0] = 3;
   g_dec_last[1] = kDecBN;
   g_dec_last[2] = p.grid;
-  g_dec_last[3] = 1;
+  g_dec_last[3] = p.cluster;
   g_dec_last[4] = stages;
   g_dec_last[5] = p.m_tiles;
   g_dec_last[6] = 1;
   g_dec_last[7] = p.k_blocks;
-  return launch_stages<5>(p, tmW, tmX, a.stream);
+  // the arena's A-row map when the pool has one (else a dummy: the tensor-core shrink is then off)
+  p.tc_shrink = (a.amap != nullptr && env_int("BDLORA_DEC_TC_SHRINK", 1) != 0) ? 1 : 0;
+  const CUtensorMap& tmA = a.amap ? *a.amap : tmX;
+  if (p.cluster > 1)
+    return deep ? launch_stages<8, true>(p, tmW, tmX, tmA, a.stream) : launch_stages<4, true>(p, tmW, tmX, tmA, a.stream);
+  return deep ? launch_stages<8, false>(p, tmW, tmX, tmA, a.stream) : launch_stages<5, false>(p, tmW, tmX, tmA, a.stream);
 }
 
 }  // namespace bdl

@@ -1,6 +1,7 @@
 // decode.h -- host interface of the lean decode kernel (kernels_decode.cuh), compiled in its own
 // translation unit (decode.cu) and called by runtime.cu.  C++ linkage, library-internal.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 
@@ -24,6 +25,7 @@ struct DecLaunch {
   cudaStream_t stream;
   int pdl;
   int lora;                   // 1 K-local, 2 v precomputed
+  const CUtensorMap* amap;    // the pool arena as [rows, K] bf16 with 16-row boxes (tensor-core K-local shrink), or null
 };
 
 constexpr int kDecMaxT = 16;

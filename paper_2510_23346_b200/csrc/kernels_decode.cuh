@@ -36,6 +36,7 @@ constexpr int kDecBM = 128, kDecBK = 64, kDecBN = 16;
 constexpr int kDecLoraRows = 32;   // K-local: sum over the batch's distinct adapters of their local rank rs
 constexpr int kDecMaxGroups = 16;  // distinct adapters of a <= 16-token batch
 constexpr int kDecMaxGrid = 1024;  // split-tile counters (indexed by the first contributor CTA)
+constexpr int kDecMaxCluster = 16; // cluster split-K: contributors of one tile (non-portable size above 8)
 
 struct DecParams {
   int M, K, T;
@@ -47,31 +48,43 @@ struct DecParams {
   Geom g;
   const float* v;     // lora == 2: v [C][T][J][Rc] fp32
   __nv_bfloat16* Y;
-  float* part;        // [grid][2][16][128] fp32 split-tile partials (slot 0: a CTA's first segment, 1: its last)
+  float* part;        // [grid][2][128][16] fp32 split-tile partials (slot 0: a CTA's first segment, 1: its last)
   int* cnt;           // [kDecMaxGrid] arrival counters of split tiles, zero between launches
   int lora;           // 0 none, 1 K-local, 2 v precomputed
   int pdl;
   int nstages;
+  int cluster;        // > 1: the tile's contributors are one thread-block cluster (DSMEM reduce, CL instantiation)
+  int tc_shrink;      // CL: the K-local shrink may run on the tensor cores (tmA = the arena's 16-row A boxes)
   long long* trace;   // optional per-CTA %globaltimer stamps (32 per CTA)
 };
 
-template <int S>
+template <int S, bool CL>
 struct DecSmem {
   static constexpr int kW = kDecBM * kDecBK * 2;  // 16 KB weight tile
   static constexpr int kX = kDecBN * kDecBK * 2;  // 2 KB token tile
-  static constexpr int kXOff = S * kW;
+  // CL: a 16-row box of the batch's adapter A rows per stage (tensor-core K-local shrink).  The ring sits
+  // FIRST: the shrink MMA's operand is 128 rows (M = 128), rows 16..127 -- ignored TMEM lanes -- read the
+  // next 14 KB of this CTA's own shared memory (following boxes and the weight ring), never past it
+  static constexpr int kA = CL ? 16 * kDecBK * 2 : 0;
+  static constexpr int kWOff = S * kA;
+  static constexpr int kXOff = kWOff + S * kW;
   static constexpr int kBarOff = kXOff + S * kX;
   static constexpr int kMiscOff = kBarOff + 256;
   // misc ints: [0,16) ids  [16,32) group of token  [32,48) group adapter  [48,64) group rs  [64,80) group row
   // offset q0  [80,96) member masks  [96] n_groups  [97] rows total ; floats [128,144) group scale ;
   // long long [160 + 2*(g*3 + j)) group A / B offsets per slice (as int pairs)
-  static constexpr int kMiscBytes = 2048;
+  static constexpr int kMiscBytes = 3584;
   static constexpr int kVsOff = kMiscOff + kMiscBytes;          // v_seg [16 tokens][3 slices][32] fp32
   static constexpr int kVsBytes = kDecBN * 3 * kDecLoraRows * 4;
   static constexpr int kBOff = kVsOff + kVsBytes;               // B rows [32][128] bf16 of the tile's columns
   static constexpr int kBBytes = kDecLoraRows * kDecBM * 2;
-  static constexpr int kBytes = kBOff + kBBytes + 1024;         // + 1024-B alignment slack
-  static_assert(kBytes <= 113 * 1024, "two CTAs per SM");
+  // cluster split-K: [s][ceil(128/s)][16] fp32 partial slots the peers push into (<= (128 + s) x 16 floats)
+  static constexpr int kSlotOff = kBOff + kBBytes;
+  static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * kDecBN * 4 : 0;
+  static constexpr int kBytes = kSlotOff + kSlotBytes + 1024;   // + 1024-B alignment slack
+  static constexpr int kTmemCols = CL ? 64 : 32;                // [acc 0 | acc 1 | v_seg (CL)]
+  static_assert(S > 5 || kBytes <= 113 * 1024, "two CTAs per SM");
+  static_assert(kBytes <= 227 * 1024, "shared memory per CTA");
 };
 
 #define DEC_TRACE(slot)                                               \
@@ -95,14 +108,61 @@ __device__ __forceinline__ int dec_slice_of(const Geom& g, int n) {
   return j;
 }
 
-template <int S>
-__global__ void __launch_bounds__(kDecThreads, 2)
+// lora == 2 (v precomputed): lr[t] = s_a v[t] . B_a[:, n] for every token of the batch (matmul_4 / _6 after
+// S-LoRA's collective).  Out of line: it runs once per output element on the S-LoRA path only, and keeping
+// it out of the kernel body keeps the decode kernel's executed footprint small.
+__device__ __noinline__ void dec_vmode_lr(const DecParams* pp, int n, float* lr) {
+  const DecParams& p = *pp;
+  for (int t = 0; t < p.T; ++t) {
+    const int a = __ldg(p.ids + t);
+    lr[t] = (a >= 0) ? lora_expand_term(t, n, a, p.tab, p.arena, p.g, p.v, p.T) : 0.f;
+  }
+}
+
+// B rows of output column n = tile * 128 + row for every group of the batch: s_B[q][row] (bf16 bits), q = the
+// group's rank-row offset + k.  Out of line (called once per tile): keeps the kernel's executed code small.
+__device__ __noinline__ void dec_stage_B(const DecParams* pp, int tile, int row, int lrows, int ngroups,
+                                         const int* s_gq0, const long long* s_goff, uint16_t* s_B) {
+  const DecParams& p = *pp;
+  const int n = tile * kDecBM + row;
+  const int jn = dec_slice_of(p.g, min(n, p.M - 1));
+  const int lo = p.g.e_lo[jn], hi = p.g.e_hi[jn], ldb = hi - lo;
+  const bool in = n < p.M && n >= lo && n < hi;
+  for (int q0 = 0; q0 < lrows; q0 += 8) {  // 8 independent loads in flight, then 8 stores
+    uint16_t b[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int q = q0 + e;
+      b[e] = 0;
+      if (q < lrows && in) {
+        int g = 0;
+        while (g + 1 < ngroups && s_gq0[g + 1] <= q) ++g;
+        const uint16_t* Bp = reinterpret_cast<const uint16_t*>(p.arena + s_goff[g * 6 + 3 + jn]);
+        b[e] = __ldg(Bp + (size_t)(q - s_gq0[g]) * ldb + (n - lo));
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (q0 + e < lrows) s_B[(q0 + e) * kDecBM + row] = b[e];
+  }
+}
+
+// v_seg[t][j] . B_{a,j}[:, n] over the adapter's rs rank rows (K-local expand of one token)
+__device__ __forceinline__ float dec_dot(const float* vs, const uint16_t* sb, int rs) {
+  float s0 = 0.f;
+  for (int k = 0; k < rs; ++k) s0 = fmaf(vs[k], bf16_bits_to_f32(sb[k * kDecBM]), s0);
+  return s0;
+}
+
+template <int S, bool CL>
+__global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
     dec_lora_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                         const DecParams p) {
-  using L = DecSmem<S>;
+                         const __grid_constant__ CUtensorMap tmA, const __grid_constant__ DecParams p) {
+  using L = DecSmem<S, CL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* sW = smem;
+  uint8_t* sA = smem;
+  uint8_t* sW = smem + L::kWOff;
   uint8_t* sX = smem + L::kXOff;
   uint64_t* full = (uint64_t*)(smem + L::kBarOff);
   uint64_t* empty = full + S;
@@ -120,6 +180,9 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   float* s_gsc = (float*)(mi + 128);
   long long* s_goff = (long long*)(mi + 160);  // [g][0..2] = offA[j], [g][3..5] = offB[j]
   float* s_vs = (float*)(smem + L::kVsOff);
+  float* s_red = (float*)(mi + 512);             // [4 warps][32] cross-warp partial dots
+  int* s_gtok = mi + 640;                         // [group][16] member tokens in token order
+  int* s_tcflag = mi + 900;                       // producer's tensor-core-shrink decision (read by the MMA warp)
   uint16_t* s_B = (uint16_t*)(smem + L::kBOff);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -127,7 +190,14 @@ __global__ void __launch_bounds__(kDecThreads, 2)
   const int UNITS = p.units, GRID = p.grid;
   const int u_lo = dec_u_lo(cta, UNITS, GRID);
   const int u_hi = dec_u_lo(cta + 1, UNITS, GRID);
-  if (threadIdx.x == 0) DEC_TRACE(0);
+  if (threadIdx.x == 0) {
+    DEC_TRACE(0);
+    if (p.trace) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      p.trace[(size_t)blockIdx.x * 32 + 31] = smid;
+    }
+  }
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmW);
@@ -143,11 +213,14 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
-  if (warp == 1) ptx::tmem_alloc<32>(tmem_holder);
+  if (warp == 1) ptx::tmem_alloc<L::kTmemCols>(tmem_holder);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  // cluster split-K: a CTA may write a peer's shared memory only once the peer runs -- arrive now, wait
+  // before the first push (long after: free)
+  if (CL) ptx::cluster_arrive_relaxed();
   // the next kernel may launch now: it only takes SM room this grid leaves free, and waits for this grid's
   // completion (griddepcontrol.wait) before touching anything this grid writes
   if (threadIdx.x == 0) ptx::pdl_launch_dependents();
@@ -167,6 +240,41 @@ __global__ void __launch_bounds__(kDecThreads, 2)
         ptx::tma_load_2d(sW + idx * L::kW, &tmW, &full[idx], kb * kDecBK, tile * kDecBM, pol_w);
       }
       DEC_TRACE(1);
+      // Tensor-core K-local shrink (CL): when the batch holds ONE adapter (plus id -1 tokens) of local rank
+      // <= 16 and the tile lies in one slice, that adapter's 16-row A box of the same K block rides every
+      // stage and the MMA warp accumulates v_seg = A_seg X_seg^T in TMEM.  Same rule as the epilogue's.
+      // ids and the slot table are read before the dependency (bdlora_set_pdl contract).
+      bool use_tc = false;
+      int arow = 0;
+      if (CL && p.lora == 1 && p.tc_shrink && nu > 0) {
+        int ids_r[kDecBN];
+#pragma unroll
+        for (int t = 0; t < kDecBN; ++t) ids_r[t] = t < p.T ? __ldg(p.ids + t) : -1;
+        int a = -1;
+        bool single = true;
+#pragma unroll
+        for (int t = 0; t < kDecBN; ++t)
+          if (ids_r[t] >= 0) {
+            if (a < 0) a = ids_r[t];
+            else if (ids_r[t] != a) single = false;
+          }
+        const int n0 = (u_lo / p.k_blocks) * kDecBM;
+        const int jlo = dec_slice_of(p.g, n0), jhi = dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
+        if (single && a >= 0 && jlo == jhi) {
+          const SlotEntry e = p.tab[a];
+          if (e.rs <= 16) {
+            use_tc = true;
+            arow = (int)(e.offA[jlo] / p.K);
+          }
+        }
+        if (use_tc)
+          for (int idx = 0; idx < P; ++idx) {
+            const int u = u_lo + idx, kb = u - (u / p.k_blocks) * p.k_blocks;
+            ptx::mbar_expect_tx(&full[idx], L::kA);
+            ptx::tma_load_2d(sA + idx * L::kA, &tmA, &full[idx], kb * kDecBK, arow, pol_x);
+          }
+      }
+      *s_tcflag = use_tc ? 1 : 0;  // published to the MMA warp by the arrivals on full[] below
       if (p.pdl) ptx::pdl_wait();
       for (int idx = 0; idx < P; ++idx) {
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks;
@@ -179,9 +287,10 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       for (int idx = P; idx < nu; ++idx) {
         const int u = u_lo + idx, tile = u / p.k_blocks, kb = u - tile * p.k_blocks;
         ptx::mbar_wait(&empty[stage], phase ^ 1);
-        ptx::mbar_arrive_expect_tx(&full[stage], L::kW + L::kX);
+        ptx::mbar_arrive_expect_tx(&full[stage], L::kW + L::kX + (use_tc ? L::kA : 0));
         ptx::tma_load_2d(sW + stage * L::kW, &tmW, &full[stage], kb * kDecBK, tile * kDecBM, pol_w);
         ptx::tma_load_2d(sX + stage * L::kX, &tmX, &full[stage], kb * kDecBK, 0, pol_x);
+        if (use_tc) ptx::tma_load_2d(sA + stage * L::kA, &tmA, &full[stage], kb * kDecBK, arow, pol_x);
         if (++stage == NS) {
           stage = 0;
           phase ^= 1;
@@ -212,6 +321,12 @@ __global__ void __launch_bounds__(kDecThreads, 2)
 #pragma unroll
           for (int k = 0; k < kDecBK / 16; ++k)
             ptx::mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          if (CL && *s_tcflag) {  // K-local shrink: V[k][t] += A_a[k][kb] . X[t][kb]  (lanes >= r/N ignored)
+            const uint64_t s_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * L::kA));
+#pragma unroll
+            for (int k = 0; k < kDecBK / 16; ++k)
+              ptx::mma_bf16(tmem_base + 32u, s_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
           ptx::mma_commit(&empty[stage]);
           if (++stage == p.nstages) {
             stage = 0;
@@ -231,8 +346,11 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     const int etid = threadIdx.x - 64;
     const int we = etid >> 5;  // epilogue warp 0..3
     const int T = p.T;
-    if (p.pdl) ptx::pdl_wait();  // X, ids (and v) of the preceding kernel are visible; orders our Y writes
     // ---- adapter groups of the batch (distinct ids, order of first appearance) -------------------------
+    // Read BEFORE the programmatic-dependency wait: ids, the slot table and the adapter factors are not
+    // written by the kernel immediately preceding a forward (include/bdlora.h, bdlora_set_pdl), so the LoRA
+    // metadata, the first tile's B rows and an L2 prefetch of the first segment's A rows all overlap the
+    // preceding kernel's tail; after the wait only X (L2-resident) is still to be read.
     if (p.lora == 1) {
       if (we == 0) {
         // lane t < T holds token t's id; leaders (first token of each id) in token order define the groups
@@ -279,10 +397,15 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           s_gq0[gidx] = incl - rs;
         }
         const int ng = __popc(lmask);
-        for (int gg = 0; gg < ng; ++gg) {  // member mask of every group (warp-uniform loop)
-          const int target = __shfl_sync(0xffffffffu, id, __fns(lmask, 0, gg + 1));
-          const unsigned m = __ballot_sync(0xffffffffu, id >= 0 && id == target);
+        unsigned lrest = lmask;
+        for (int gg = 0; gg < ng; ++gg) {  // member mask and member list of every group (warp-uniform loop)
+          const int leader = __ffs(lrest) - 1;
+          lrest &= lrest - 1;
+          const int target = __shfl_sync(0xffffffffu, id, leader);
+          const bool mem = id >= 0 && id == target;
+          const unsigned m = __ballot_sync(0xffffffffu, mem);
           if (lane == 0) s_gmask[gg] = (int)m;
+          if (mem) s_gtok[gg * 16 + __popc(m & ((1u << lane) - 1u))] = lane;
         }
         if (lane == 0) {
           mi[96] = ng;
@@ -292,10 +415,33 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       ptx::named_bar_sync(1, 128);
     }
     const int ngroups = (p.lora == 1) ? mi[96] : 0;
+    const int lrows = (p.lora == 1) ? mi[97] : 0;
+    int cur_tile = -1;
+    auto stage_B = [&](int tile) {
+      dec_stage_B(&p, tile, row, lrows, ngroups, s_gq0, s_goff, s_B);
+      cur_tile = tile;
+    };
+    if (p.lora == 1 && ngroups > 0 && u_lo < u_hi) {
+      const int tile = u_lo / p.k_blocks, kb0 = u_lo - tile * p.k_blocks;
+      const int kb1 = min(p.k_blocks, kb0 + (u_hi - u_lo));
+      stage_B(tile);
+      // L2 prefetch of the first segment's A rows (one bulk prefetch per row and slice)
+      const int n0 = tile * kDecBM;
+      const int jlo = dec_slice_of(p.g, n0), jhi = dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
+      const int d_lo = kb0 * kDecBK, d_hi = min(p.K, kb1 * kDecBK);
+      for (int it = etid; it < (jhi - jlo + 1) * lrows; it += 128) {
+        const int jj = it / lrows, q = it - jj * lrows;
+        int g = 0;
+        while (g + 1 < ngroups && s_gq0[g + 1] <= q) ++g;
+        ptx::prefetch_l2_bulk(p.arena + s_goff[g * 6 + jlo + jj] + (size_t)(q - s_gq0[g]) * p.K + d_lo,
+                              (uint32_t)(d_hi - d_lo) * 2);
+      }
+    }
+    if (p.pdl) ptx::pdl_wait();  // X (and v) of the preceding kernel are visible; orders our Y writes
+    long long vs_key = -1;       // (slice range, K range) whose v_seg s_vs holds
 
     int acc = 0;
     uint32_t acc_phase = 0;
-    int cur_tile = -1;
     for (int u = u_lo; u < u_hi;) {
       const int tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks;
@@ -308,77 +454,117 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       float lr[kDecBN];
 #pragma unroll
       for (int i = 0; i < kDecBN; ++i) lr[i] = 0.f;
-      if (p.lora == 1 && ngroups > 0) {
+      // tensor-core K-local shrink taken by the producer (same rule): v_seg arrives in TMEM with the accumulator
+      const bool tc = CL && p.tc_shrink && p.lora == 1 && ngroups == 1 && s_grs[0] <= 16 &&
+                      jlo == dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
+      if (p.lora == 1 && ngroups > 0 && !tc) {
         // ---- K-local shrink of this segment: v_seg[t][j][k] = s_a sum_{d in seg} X[t][d] A_{a,j}[k][d] -----
+        // Thread per 16-byte chunk of the K range, 8 rank rows x 4 tokens per pass: 12 independent loads in
+        // flight per chunk (the A rows are L2-resident, X was just written by the preceding kernel), then a
+        // fixed-order reduction over the 128 threads.  Whole tiles of one slice reuse the previous v_seg.
         const int jhi = dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
         const int nj = jhi - jlo + 1;
-        const int rows = mi[97];
         const int d_lo = kb0 * kDecBK, d_hi = min(p.K, kb1 * kDecBK);
+        const long long key = (((long long)(jlo * 4 + nj) * 65536 + kb0) * 65536) + kb1;
         ptx::named_bar_sync(1, 128);  // previous segment's readers of s_vs / s_B are done
-        for (int item = we; item < nj * rows; item += 4) {
-          const int jj = item / rows, q = item - jj * rows;
-          int g = 0;
-          while (g + 1 < ngroups && s_gq0[g + 1] <= q) ++g;
-          const int k = q - s_gq0[g];
-          const int j = jlo + jj;
-          const unsigned mask = (unsigned)s_gmask[g];
-          const __nv_bfloat16* Ar = p.arena + s_goff[g * 6 + j] + (size_t)k * p.K;
-          float a16[kDecBN];
+        if (key != vs_key) {
+          vs_key = key;
+          const int nch = (d_hi - d_lo) >> 3;
+#pragma unroll 1
+          for (int jj = 0; jj < nj; ++jj) {
+#pragma unroll 1
+            for (int g = 0; g < ngroups; ++g) {
+              const unsigned gm = (unsigned)s_gmask[g];
+              const int R = s_grs[g], ntok = __popc(gm);
+              const float sc = s_gsc[g];
+              const __nv_bfloat16* Ag = p.arena + s_goff[g * 6 + jlo + jj];
+#pragma unroll 1
+              for (int rb = 0; rb < R; rb += 8) {
+#pragma unroll 1
+                for (int tb = 0; tb < ntok; tb += 4) {
+                  // rows past R and tokens past the group re-read a valid row / token (an L1 hit) and are
+                  // dropped at the write: the loop body has no data-dependent branches (one code version)
+                  int tok[4];
+                  const __nv_bfloat16* xr[4];
+                  const __nv_bfloat16* ar[8];
 #pragma unroll
-          for (int t = 0; t < kDecBN; ++t) a16[t] = 0.f;
-          for (int d = d_lo + lane * 8; d < d_hi; d += 256) {
-            float af[8];
-            bf16x8_to_f32(ld_cached_u4(Ar + d), af);
+                  for (int qq = 0; qq < 4; ++qq) {
+                    tok[qq] = (tb + qq < ntok) ? s_gtok[g * 16 + tb + qq] : -1;
+                    xr[qq] = p.X + (size_t)(tok[qq] >= 0 ? tok[qq] : s_gtok[g * 16]) * p.K + d_lo;
+                  }
 #pragma unroll
-            for (int t = 0; t < kDecBN; ++t) {
-              if ((mask >> t) & 1u) {
-                float xf[8];
-                bf16x8_to_f32(ld_cached_u4(p.X + (size_t)t * p.K + d), xf);
+                  for (int r = 0; r < 8; ++r) ar[r] = Ag + (size_t)min(rb + r, R - 1) * p.K + d_lo;
+                  float a32[8][4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) a16[t] = fmaf(af[e], xf[e], a16[t]);
+                  for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) a32[r][qq] = 0.f;
+#pragma unroll 1
+                  for (int c = etid; c < nch; c += 128) {
+                    uint4 av[8], xv[4];
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) av[r] = ld_cached_u4(ar[r] + c * 8);
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) xv[qq] = ld_cached_u4(xr[qq] + c * 8);
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) {
+                      float xf[8];
+                      bf16x8_to_f32(xv[qq], xf);
+#pragma unroll
+                      for (int r = 0; r < 8; ++r) {
+                        float af[8];
+                        bf16x8_to_f32(av[r], af);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) a32[r][qq] = fmaf(af[e], xf[e], a32[r][qq]);
+                      }
+                    }
+                  }
+                  // transpose reduction over the warp: after 5 halving steps (31 shuffles) lane l holds the
+                  // warp's sum of value l = r * 4 + qq
+                  float vv[32];
+#pragma unroll
+                  for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) vv[r * 4 + qq] = a32[r][qq];
+#pragma unroll
+                  for (int o = 16, c = 32; o >= 1; o >>= 1, c >>= 1) {
+                    const bool up = (lane & o) != 0;
+#pragma unroll
+                    for (int i = 0; i < c / 2; ++i) {
+                      const float send = up ? vv[i] : vv[i + c / 2];
+                      const float keep = up ? vv[i + c / 2] : vv[i];
+                      vv[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                    }
+                  }
+                  s_red[we * 32 + lane] = vv[0];
+                  ptx::named_bar_sync(1, 128);
+                  if (etid < 32) {
+                    const int r = etid >> 2, qq = etid & 3;
+                    if (rb + r < R && tok[qq] >= 0) {
+                      const float sm = (s_red[etid] + s_red[32 + etid]) + (s_red[64 + etid] + s_red[96 + etid]);
+                      s_vs[(tok[qq] * 3 + jj) * kDecLoraRows + rb + r] = sc * sm;
+                    }
+                  }
+                  ptx::named_bar_sync(1, 128);  // s_red free again
+                }
               }
             }
           }
-          const float sc = s_gsc[g];
-#pragma unroll
-          for (int t = 0; t < kDecBN; ++t) {
-            if ((mask >> t) & 1u) {
-              const float sm = warp_sum(a16[t]);
-              if (lane == 0) s_vs[(t * 3 + jj) * kDecLoraRows + k] = sc * sm;
-            }
-          }
         }
-        // ---- B rows of my output column for every group (once per tile): s_B[q][row] ----------------------
-        if (tile != cur_tile) {
-          const int lo = p.g.e_lo[jn], hi = p.g.e_hi[jn], ldb = hi - lo;
-          const bool in = n < p.M && n >= lo && n < hi;
-          for (int q = 0; q < rows; ++q) {
-            int g = 0;
-            while (g + 1 < ngroups && s_gq0[g + 1] <= q) ++g;
-            const int k = q - s_gq0[g];
-            const uint16_t* Bp = reinterpret_cast<const uint16_t*>(p.arena + s_goff[g * 6 + 3 + jn]);
-            s_B[q * kDecBM + row] = in ? __ldg(Bp + (size_t)k * ldb + (n - lo)) : (uint16_t)0;
-          }
-          cur_tile = tile;
-        }
+        if (tile != cur_tile) stage_B(tile);
         ptx::named_bar_sync(1, 128);
         // ---- expand: lr[t] = v_seg[t][j] . B_{a(t),j}[:, n] ---------------------------------------------
         const int jj = jn - jlo;
+        if (T == 1) {  // straight-line batch-1 path (see the tensor-core expand below)
+          const int g = s_grp[0];
+          if (g >= 0) lr[0] = dec_dot(s_vs + jj * kDecLoraRows, s_B + s_gq0[g] * kDecBM + row, s_grs[g]);
+        } else {
 #pragma unroll
-        for (int t = 0; t < kDecBN; ++t) {
-          if (t < T) {
-            const int g = s_grp[t];
-            if (g >= 0) {
-              const int rs = s_grs[g], q0 = s_gq0[g];
-              const float* vs = s_vs + (t * 3 + jj) * kDecLoraRows;
-              float s0 = 0.f, s1 = 0.f;
-              int k = 0;
-              for (; k + 1 < rs; k += 2) {
-                s0 = fmaf(vs[k], bf16_bits_to_f32(s_B[(q0 + k) * kDecBM + row]), s0);
-                s1 = fmaf(vs[k + 1], bf16_bits_to_f32(s_B[(q0 + k + 1) * kDecBM + row]), s1);
-              }
-              if (k < rs) s0 = fmaf(vs[k], bf16_bits_to_f32(s_B[(q0 + k) * kDecBM + row]), s0);
-              lr[t] = s0 + s1;
+          for (int t = 0; t < kDecBN; ++t) {
+            if (t < T) {
+              const int g = s_grp[t];
+              if (g >= 0)
+                lr[t] = dec_dot(s_vs + (t * 3 + jj) * kDecLoraRows, s_B + s_gq0[g] * kDecBM + row, s_grs[g]);
             }
           }
         }
@@ -391,12 +577,87 @@ __global__ void __launch_bounds__(kDecThreads, 2)
       ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * kDecBN), r);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);  // the accumulator is in registers: the MMA may reuse it
-      if (whole) {
-        if (p.lora == 2 && n < p.M) {
+      if (tc) {
+        // v_seg (TMEM lanes k < r/N of the shrink accumulator, read by the lane-quarter-0 warp) -> s_vs, then
+        // lr[t] = s v_seg[t] . B[:, n] for the adapter's tokens (B rows staged before the dependency wait)
+        if (q4 == 0) {
+          uint32_t v16[16];
+          ptx::tmem_ld_32x32b_x16(tmem_base + 32u, v16);
+          ptx::tmem_ld_wait();
+          const int rs = s_grs[0];
+          const float sc = s_gsc[0];
+          if (lane < rs) {
+#pragma unroll
+            for (int t = 0; t < kDecBN; ++t) s_vs[(t * 3) * kDecLoraRows + lane] = sc * __uint_as_float(v16[t]);
+          }
+        }
+        ptx::named_bar_sync(1, 128);
+        if (etid == 0) DEC_TRACE(9);
+        // batch 1 (the common decode case) takes a straight-line path: the 16-way guarded unroll below jumps
+        // over 15 cold code blocks (instruction-cache misses on the critical tail)
+        if (T == 1) {
+          if (s_grp[0] == 0) lr[0] = dec_dot(s_vs, s_B + row, s_grs[0]);
+        } else {
 #pragma unroll
           for (int t = 0; t < kDecBN; ++t)
-            if (t < T) lr[t] = lora_expand_term(t, n, __ldg(p.ids + t), p.tab, p.arena, p.g, p.v, T);
+            if (t < T && s_grp[t] == 0) lr[t] = dec_dot(s_vs + (t * 3) * kDecLoraRows, s_B + row, s_grs[0]);
+        }
+        if (etid == 0) DEC_TRACE(10);
+      }
+      ptx::mbar_arrive(&tempty[acc]);  // the accumulator is in registers: the MMA may reuse it
+      if (CL) {
+        // ---- cluster split-K: the s contributors of this tile are this cluster.  Rank c owns rows
+        // [c*128/s, (c+1)*128/s): every contributor pushes its partial rows into the owner's slots (DSMEM,
+        // st.shared::cluster), one cluster barrier, the owner sums in rank order (deterministic), rounds once
+        const int sc = p.cluster;
+        const uint32_t crank = ptx::cluster_ctarank();
+        const int nr_max = (kDecBM + sc - 1) / sc;
+        const int owner = ((row + 1) * sc - 1) / kDecBM;
+        const int rr = row - (owner * kDecBM) / sc;
+        float* s_slot = reinterpret_cast<float*>(smem + L::kSlotOff);
+        const uint32_t dst = ptx::mapa(ptx::smem_u32(s_slot + ((size_t)(crank * nr_max + rr) * kDecBN)), (uint32_t)owner);
+        const int nq = (T + 3) >> 2;
+        ptx::cluster_wait();  // (early arrival) every peer has started
+        if (etid == 0) DEC_TRACE(11);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < nq)
+            ptx::st_dsmem_f4(dst + q * 16, __uint_as_float(r[4 * q]) + lr[4 * q], __uint_as_float(r[4 * q + 1]) + lr[4 * q + 1],
+                             __uint_as_float(r[4 * q + 2]) + lr[4 * q + 2], __uint_as_float(r[4 * q + 3]) + lr[4 * q + 3]);
+        if (etid == 0) DEC_TRACE(12);
+        ptx::cluster_arrive();  // release: my pushes
+        ptx::cluster_wait();    // acquire: every peer's rows of my range
+        if (etid == 0) DEC_TRACE(6);
+        const int r_lo = (crank * kDecBM) / sc, nr = ((crank + 1) * kDecBM) / sc - r_lo;
+        for (int f = etid; f < nr * nq; f += 128) {
+          const int r2 = f % nr, qd = f / nr;
+          float4 y = *reinterpret_cast<const float4*>(s_slot + (size_t)r2 * kDecBN + qd * 4);
+          for (int c = 1; c < sc; ++c) {
+            const float4 z = *reinterpret_cast<const float4*>(s_slot + ((size_t)(c * nr_max + r2) * kDecBN + qd * 4));
+            y.x += z.x, y.y += z.y, y.z += z.z, y.w += z.w;
+          }
+          const int nn = n0 + r_lo + r2;
+          if (nn < p.M) {
+            float yv[4] = {y.x, y.y, y.z, y.w};
+            if (p.lora == 2) {
+              float lrv[kDecBN];
+              dec_vmode_lr(&p, nn, lrv);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (qd * 4 + i < T) yv[i] += lrv[qd * 4 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (qd * 4 + i < T) p.Y[(size_t)(qd * 4 + i) * p.M + nn] = __float2bfloat16_rn(yv[i]);
+          }
+        }
+      } else if (whole) {
+        if (p.lora == 2 && n < p.M) {
+          float lrv[kDecBN];
+          dec_vmode_lr(&p, n, lrv);
+#pragma unroll
+          for (int t = 0; t < kDecBN; ++t)
+            if (t < T) lr[t] = lrv[t];
         }
         if (n < p.M) {
 #pragma unroll
@@ -404,12 +665,17 @@ __global__ void __launch_bounds__(kDecThreads, 2)
             if (t < T) p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[t]) + lr[t]);
         }
       } else {
-        // split tile: this CTA's fp32 partial (its K range, with its K-local LoRA share) -> slot, token-major
+        // split tile: this CTA's fp32 partial (its K range, with its K-local LoRA share) -> its slot,
+        // [row][16 tokens]: a thread's tokens are one contiguous 64-byte run (float4 stores / loads)
         const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
-        float* my = p.part + (size_t)(cta * 2 + slot) * kDecBN * kDecBM;
+        float4* my = reinterpret_cast<float4*>(p.part + ((size_t)(cta * 2 + slot) * kDecBM + row) * kDecBN);
+        const int nq = (T + 3) >> 2;
 #pragma unroll
-        for (int t = 0; t < kDecBN; ++t)
-          if (t < T) __stcg(my + t * kDecBM + row, __uint_as_float(r[t]) + lr[t]);
+        for (int q = 0; q < 4; ++q)
+          if (q < nq)
+            __stcg(my + q, make_float4(__uint_as_float(r[4 * q]) + lr[4 * q], __uint_as_float(r[4 * q + 1]) + lr[4 * q + 1],
+                                       __uint_as_float(r[4 * q + 2]) + lr[4 * q + 2],
+                                       __uint_as_float(r[4 * q + 3]) + lr[4 * q + 3]));
         ptx::named_bar_sync(1, 128);
         const int ts = tile * p.k_blocks;
         const int c_first = dec_cta_of(ts, UNITS, GRID);
@@ -423,21 +689,36 @@ __global__ void __launch_bounds__(kDecThreads, 2)
           // finisher: contributors' partials summed in CTA order (deterministic), one rounding
           if (etid == 0) DEC_TRACE(6);
           const int c_last = dec_cta_of(ts + p.k_blocks - 1, UNITS, GRID);
+          // loads of 8 contributors in flight per round, summed in CTA order
           float y[kDecBN];
 #pragma unroll
           for (int t = 0; t < kDecBN; ++t) y[t] = 0.f;
-          for (int c = c_first; c <= c_last; ++c) {
-            const int sl = (ts > dec_u_lo(c, UNITS, GRID)) ? 1 : 0;
-            const float* src = p.part + (size_t)(c * 2 + sl) * kDecBN * kDecBM + row;
 #pragma unroll
-            for (int t = 0; t < kDecBN; ++t)
-              if (t < T) y[t] += __ldcg(src + t * kDecBM);
+          for (int q = 0; q < 4; ++q) {
+            if (q < nq) {
+              float4 yq = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int cb = c_first; cb <= c_last; cb += 8) {
+                float4 b8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int c = min(cb + e, c_last);
+                  const int sl = (ts > dec_u_lo(c, UNITS, GRID)) ? 1 : 0;
+                  b8[e] = __ldcg(reinterpret_cast<const float4*>(p.part + ((size_t)(c * 2 + sl) * kDecBM + row) * kDecBN) + q);
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  if (cb + e <= c_last) yq.x += b8[e].x, yq.y += b8[e].y, yq.z += b8[e].z, yq.w += b8[e].w;
+              }
+              y[4 * q] = yq.x, y[4 * q + 1] = yq.y, y[4 * q + 2] = yq.z, y[4 * q + 3] = yq.w;
+            }
           }
           if (n < p.M) {
             if (p.lora == 2) {
+              float lrv[kDecBN];
+              dec_vmode_lr(&p, n, lrv);
 #pragma unroll
               for (int t = 0; t < kDecBN; ++t)
-                if (t < T) y[t] += lora_expand_term(t, n, __ldg(p.ids + t), p.tab, p.arena, p.g, p.v, T);
+                if (t < T) y[t] += lrv[t];
             }
 #pragma unroll
             for (int t = 0; t < kDecBN; ++t)
@@ -453,11 +734,17 @@ __global__ void __launch_bounds__(kDecThreads, 2)
     }
     if (etid == 0) DEC_TRACE(7);
   }
+  if (warp == 0 && lane == 0) DEC_TRACE(8);  // producer done issuing
+  if (CL && warp < 2) {  // the epilogue's cluster barriers count every thread of the CTA
+    ptx::cluster_wait();
+    ptx::cluster_arrive();
+    ptx::cluster_wait();
+  }
 
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if (warp == 1) ptx::tmem_dealloc<32>(tmem_base);
+  if (warp == 1) ptx::tmem_dealloc<L::kTmemCols>(tmem_base);
 }
 
 }  // namespace bdl

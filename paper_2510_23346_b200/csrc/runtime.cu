@@ -346,6 +346,7 @@ int launch_decode(const bdlora_pool* p, const void* X, int T, const void* W, con
   a.stream = st;
   a.pdl = g_pdl;
   a.lora = lora;
+  a.amap = p->amap_ok ? &p->amap : nullptr;
   const int rc = bdl::dec_launch(a);
   if (rc < 0) return fail(BDLORA_E_CUDA, "decode kernel launch: %s", cudaGetErrorString(cudaGetLastError()));
   if (rc > 0) return -1;  // shape not handled here

@@ -32,6 +32,9 @@ DEC_VARIANTS = {
     "dec_two_stages": {"BDLORA_DEC_STAGES": "2"},
     "dec_min_4_kblocks": {"BDLORA_DEC_MINKB": "4"},
     "dec_grid_37": {"BDLORA_DEC_CTAS": "37"},
+    "dec_no_cluster_global_fixup": {"BDLORA_DEC_CLUSTER": "0"},
+    "dec_cluster_max_8": {"BDLORA_DEC_CLUSTER": "8"},
+    "dec_cuda_core_shrink": {"BDLORA_DEC_TC_SHRINK": "0"},
 }
 
 
