@@ -58,7 +58,7 @@ int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap&
   cudaGetDevice(&dev);
   dev = std::min(std::max(dev, 0), kMaxDev - 1);
   if (!attr[dev]) {
-    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) !=
+    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
         cudaSuccess)
       return -1;
     if (CL && cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
@@ -88,8 +88,10 @@ int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap&
   return cudaLaunchKernelEx(&cfg, dec_lora_gemm_kernel<S, CL>, tmW, tmX, tmA, p) == cudaSuccess ? 0 : -1;
 }
 
-// Largest cluster size <= want (>= 2) with at least `need` co-resident clusters, cached per (device, size).
-int fit_cluster(int want, int need, int grid_per_cluster_tiles) {
+// Largest cluster size c in [2, want] such that `need` clusters of instantiation <S, true> are co-resident
+// (one wave: every tile's contributors run at once), cached per (device, S, size); 1 if none.
+template <int S>
+int fit_cluster(int want, int need) {
   static int cache[kMaxDev][kDecMaxCluster + 1];
   static bool init = false;
   if (!init) {
@@ -103,12 +105,12 @@ int fit_cluster(int want, int need, int grid_per_cluster_tiles) {
   for (int c = want; c >= 2; --c) {
     int& mc = cache[dev][c];
     if (mc < 0) {
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<4, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t qc = {};
-      qc.gridDim = dim3(c * grid_per_cluster_tiles);
+      qc.gridDim = dim3(c * need);
       qc.blockDim = dim3(kDecThreads);
-      qc.dynamicSmemBytes = DecSmem<4, true>::kBytes;
+      qc.dynamicSmemBytes = DecSmem<S, true>::kBytes;
       cudaLaunchAttribute ca[1];
       ca[0].id = cudaLaunchAttributeClusterDimension;
       ca[0].val.clusterDim.x = c;
@@ -116,7 +118,7 @@ int fit_cluster(int want, int need, int grid_per_cluster_tiles) {
       ca[0].val.clusterDim.z = 1;
       qc.attrs = ca;
       qc.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<4, true>, &qc) != cudaSuccess) {
+      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<S, true>, &qc) != cudaSuccess) {
         cudaGetLastError();
         mc = 0;
       }
@@ -162,18 +164,29 @@ int dec_launch(const DecLaunch& a) {
   long long grid;
   const int min_kb = std::max(1, env_int("BDLORA_DEC_MINKB", 1));
   p.cluster = 1;
+  static const int deep_kb = env_int("BDLORA_DEC_DEEP_KB", 16);
+  bool deep = false;
   if (tiles <= sms) {
     int s = std::max(1, std::min(sms / tiles, p.k_blocks / min_kb));
     // the tile's s contributors reduce through a thread-block cluster (DSMEM) when s >= 2: the global
-    // last-arriver fix-up costs two dependent L2 round trips (atomic + partial loads, often cross-die)
+    // last-arriver fix-up costs two dependent L2 round trips (atomic + partial loads, often cross-die).
+    // Long K segments (>= deep_kb k-blocks per CTA) prefer the deep 8-stage ring if its clusters (one CTA
+    // per SM) still fit in one wave; else the 4-stage ring (two CTAs per SM)
     static const int cl_max = std::min(kDecMaxCluster, env_int("BDLORA_DEC_CLUSTER", kDecMaxCluster));
     if (s >= 2 && cl_max >= 2) {
-      const int c = fit_cluster(std::min(s, cl_max), 1, 1);
+      const int want = std::min(s, cl_max);
+      int c = 1;
+      if (deep_kb > 0 && p.k_blocks / want >= deep_kb) {
+        c = fit_cluster<8>(want, tiles);
+        deep = c >= 2;
+      }
+      if (c < 2) c = fit_cluster<4>(want, tiles);
       if (c >= 2) {
         s = c;
         p.cluster = c;
       }
     }
+    if (p.cluster == 1) deep = deep_kb > 0 && p.k_blocks / s >= deep_kb;
     grid = (long long)tiles * s;
   } else {
     grid = 0;
@@ -185,6 +198,7 @@ int dec_launch(const DecLaunch& a) {
   if (override_ctas > 0) {
     grid = std::min<long long>(override_ctas, units);
     p.cluster = 1;
+    deep = false;
   }
   grid = std::max<long long>(1, std::min<long long>(grid, units));
   if (grid > std::min(sms, kDecMaxGrid) && grid != tiles) grid = std::min(sms, kDecMaxGrid);
@@ -207,8 +221,7 @@ int dec_launch(const DecLaunch& a) {
   // Long weight streams (>= 16 k-blocks = 256 KB per CTA, e.g. TP1 / TP2 projections) take a deep 8-stage ring (one CTA
   // per SM: the PDL overlap with the next projection matters little next to a 30+ us stream); the rest keep
   // <= 113 KB so two CTAs share an SM across projection boundaries.
-  static const int deep_kb = env_int("BDLORA_DEC_DEEP_KB", 16);
-  const bool deep = deep_kb > 0 && units / p.grid >= deep_kb;
+  if (tiles > sms) deep = deep_kb > 0 && units / p.grid >= deep_kb;
   const int smax = deep ? 8 : p.cluster > 1 ? 4 : 5;
   const int stages = std::min(smax, std::max(2, env_int("BDLORA_DEC_STAGES", smax)));
   p.nstages = stages;
