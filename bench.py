@@ -205,6 +205,8 @@ class Projection:
         self.Y = torch.empty(T, m, dtype=torch.bfloat16, device=dev)
         self.ws = bd.make_workspace(self.pool, T)
 
+    peer = None  # fused row all-reduce peer group (N > 1, decode batches): bdlora_row_forward_fused
+
     def run(self, bd, comm, ids, rep, X=None, Y=None):
         X = self.X if X is None else X
         Y = self.Y if Y is None else Y
@@ -212,6 +214,8 @@ class Projection:
         if self.sharding == "bd":
             if self.proj.parallel == "column":
                 bd.bdlora_column_forward(self.pool, X, W, ids, Y, self.ws)
+            elif self.peer is not None:
+                bd.bdlora_row_forward_fused(self.pool, self.peer, X, W, ids, Y, self.ws)
             else:
                 bd.bdlora_row_forward(self.pool, comm, X, W, ids, Y, self.ws)
         elif self.sharding == "nfs":
@@ -226,6 +230,8 @@ class Projection:
                 bd.slora_row_forward(self.pool, comm, X, W, ids, Y, self.ws)
 
     def close(self):
+        if self.peer is not None:
+            self.peer.close()
         self.pool.close()
 
 
@@ -597,6 +603,11 @@ def run_ours(args, wl):
     # ---------------- BD-LoRA layer (the step) ----------------
     keep = sorted(set(int(a) for a in ids_np.tolist() if a >= 0)) if world == 1 else ()
     layer, reps = build_layer(bd, torch, wl, "bd", n, rank, dev, keep_slots=keep)
+    fused_ar = world > 1 and T <= 16 and not args.no_fused_ar
+    if fused_ar:  # the row layers' base all-reduce fused into the decode kernel over NVLink peer memory
+        for p in layer:
+            if p.proj.parallel == "row":
+                p.peer = bd.bdlora_peer_create(comm, T * p.m)
     clocks = ClockSampler(local)
     clocks.start()
     total_ms, per, launches = time_layer(bd, torch, layer, comm, ids, args.steps, args.warmup, not args.no_graph, barrier)
@@ -732,7 +743,9 @@ def run_ours(args, wl):
                        "resident_adapters": wl["n_adapters"], "sharding": "BD-LoRA",
                        "l2": f"inputs larger than L2: {reps} weight replica(s) rotated, "
                              f"{reps * layer_bytes / 1e6:.0f} MB per rotation >= 3 x 126 MB L2",
-                       "cuda_graph": not args.no_graph, "parallelism": f"tp{n}"},
+                       "cuda_graph": not args.no_graph, "parallelism": f"tp{n}",
+                       "row_allreduce": ("fused peer-memory (bdlora_row_forward_fused)" if fused_ar else
+                                         "ncclAllReduce bf16" if world > 1 else "none (N = 1)")},
             "layer_us": ms_step * 1e3, "proj_us": proj_us, "layer_hbm_frac": layer_frac,
             "layer_algorithmic_bytes": layer_bytes,
             "slora": slora, "nfs": nfs, "collectives": collectives, "tp_emulated_1gpu": tp_emulated,
@@ -868,6 +881,8 @@ def main():
     ap.add_argument("--skip-slora", action="store_true", help="skip the S-LoRA and NFS-LoRA comparison legs")
     ap.add_argument("--skip-tp-emulation", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--no-fused-ar", action="store_true",
+                    help="N > 1: BD row layers all-reduce with NCCL instead of the fused peer-memory path")
     ap.add_argument("--decode-layers", type=int, default=None,
                     help="layers of the whole-decode-step leg (batch-1 workloads; default: the model's depth; 0 = off)")
     args = ap.parse_args()

@@ -55,6 +55,7 @@ extern "C" {
 
 typedef struct bdlora_pool bdlora_pool; /* opaque: one per (device, projection, sharding mode)  */
 typedef struct bdlora_comm bdlora_comm; /* opaque: wraps an ncclComm_t owned by the library      */
+typedef struct bdlora_peer bdlora_peer; /* opaque: peer-mapped receive buffers of the fused AR  */
 typedef void* bdlora_stream_t;          /* cudaStream_t                                          */
 
 typedef enum {
@@ -143,6 +144,40 @@ int bdlora_comm_destroy(bdlora_comm* comm);
    [3] base all-reduce bytes, [4] LoRA all-gather bytes (per rank, sent), [5] LoRA all-reduce bytes.
    BD-LoRA paths never touch counts[1], [2], [4], [5] (Fig. 3 caption).               */
 int bdlora_comm_stats(const bdlora_comm* comm, int64_t counts[6]);
+
+/* ---------------------------------------------------------------- fused row all-reduce ------ */
+/* the row-parallel layer's base all-reduce (Alg. 1 line 15) fused with
+   the GEMM.  A peer group maps every rank's receive buffer ([2 parities][N sources][max_elems] fp32) and
+   arrival counters into every rank's address space (CUDA IPC over NVLink / NVSwitch).  The decode kernel's
+   epilogue writes its fp32 row partial P_i straight into slot [parity][i] of EVERY rank's buffer (peer
+   stores, tile by tile as the tiles finish) and each CTA then signals every rank with a system-scope
+   release; a small reduce kernel on each rank waits for N x grid arrivals and sums the N slots IN RANK
+   ORDER in fp32, rounding once to bf16 -- every rank gets the same bits, and the sum is more accurate
+   than the bf16 NCCL reduction of bdlora_row_forward (reading R7: rounding once).  No NCCL launch.
+   Decode batches only (T <= 16 with the decode kernel's K-local LoRA capacity; else E_CAPACITY: use
+   bdlora_row_forward).  BD and NFS row pools (S-LoRA keeps its NCCL collectives: E_MODE).
+   Calls on one peer group must be issued in the same order on every rank (call parity alternates);
+   push and reduce of one rank must not be separated by another push on the same group.                */
+/* Collective over `comm` (every rank calls it): allocates this rank's buffers (2 x nranks x max_elems
+   fp32; max_elems >= T x d_out of any call) and exchanges IPC handles through the communicator.        */
+int bdlora_peer_create(bdlora_comm* comm, int64_t max_elems, bdlora_peer** out);
+/* Test / emulation: `nranks` peer groups of one process on ONE device (out[r] = rank r), mapping each
+   other's buffers directly.  Issue every rank's push before any rank's reduce (a reduce that waits for a
+   push queued behind it on the same stream would spin; after ~2 s it gives up and flags an error).     */
+int bdlora_peer_create_local(int nranks, int cuda_device, int64_t max_elems, bdlora_peer** out);
+int bdlora_peer_destroy(bdlora_peer* peer);
+/* 1 if a reduce gave up waiting for peers (~2 s), else 0 (synchronises the device).                   */
+int bdlora_peer_error(const bdlora_peer* peer, int32_t* err);
+/* Phase 1: P_i = X_i W_i + s (X_i A_i[a]) B_i[a] (Alg. 1 lines 9-12) computed by the decode kernel and
+   pushed, fp32, into every rank's receive slot.  X [T, d_in/N], W = W_i^T [d_out, d_in/N], ids [T].    */
+int bdlora_row_partial_push(bdlora_pool* pool, bdlora_peer* peer, const void* X, int64_t T, const void* W,
+                            const int32_t* ids, void* workspace, size_t ws_bytes, bdlora_stream_t stream);
+/* Phase 2: Y [T, M] bf16 = sum over ranks of the pushed partials (M = d_out), once all have arrived.     */
+int bdlora_peer_reduce(bdlora_peer* peer, void* Y, int64_t T, int32_t M, bdlora_stream_t stream);
+/* Both phases: Y = AllReduce_i(P_i), replicated on every rank (Alg. 1 end to end).         */
+int bdlora_row_forward_fused(bdlora_pool* pool, bdlora_peer* peer, const void* X, int64_t T, const void* W,
+                             const int32_t* ids, void* Y, void* workspace, size_t ws_bytes,
+                             bdlora_stream_t stream);
 
 /* ---------------------------------------------------------------- adapter pool -------------- */
 int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_pool** out);

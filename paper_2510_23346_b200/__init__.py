@@ -28,7 +28,9 @@ __all__ = [
     "bdlora_load_adapter", "bdlora_unload_adapter", "bdlora_pool_bytes", "bdlora_pool_geometry",
     "bdlora_workspace_bytes", "bdlora_build_segments", "bdlora_column_forward", "bdlora_row_partial",
     "bdlora_row_forward", "slora_column_forward", "slora_row_forward", "bdlora_lora_shrink",
-    "bdlora_base_expand", "bdlora_v_elems", "make_workspace", "bdlora_workspace_init", "bdlora_last_launch_info", "bdlora_set_decode_lora", "bdlora_load_adapter_blocks",
+    "bdlora_base_expand", "bdlora_v_elems", "make_workspace", "bdlora_workspace_init", "bdlora_last_launch_info",
+    "Peer", "bdlora_peer_create", "bdlora_peer_create_local", "bdlora_peer_error", "bdlora_row_partial_push",
+    "bdlora_peer_reduce", "bdlora_row_forward_fused", "bdlora_set_decode_lora", "bdlora_load_adapter_blocks",
 ]
 
 
@@ -103,6 +105,18 @@ class Comm:
     def close(self):
         if self.handle:
             call("bdlora_comm_destroy", self.handle)
+            self.handle = None
+
+
+class Peer:
+    """Owning handle of a bdlora_peer (fused row all-reduce peer group, include/bdlora.h)."""
+
+    def __init__(self, handle: int, rank: int, nranks: int, device: int):
+        self.handle, self.rank, self.nranks, self.device = handle, rank, nranks, device
+
+    def close(self):
+        if self.handle:
+            call("bdlora_peer_destroy", self.handle)
             self.handle = None
 
 
@@ -375,6 +389,52 @@ def nfs_row_partial(pool: Pool, X, W, ids, P, ws, stream=None) -> None:
 def nfs_row_forward(pool: Pool, comm: Optional[Comm], X, W, ids, Y, ws, stream=None) -> None:
     T = _check_fwd(pool, X, W, ids, Y, ws, pool.k_loc, pool.m_loc)
     call("nfs_row_forward", pool.handle, _comm_ptr(comm), _ptr(X), T, _ptr(W), _ptr(ids), _ptr(Y), _ptr(ws),
+         ws.numel(), _stream(stream))
+
+
+def bdlora_peer_create(comm: Comm, max_elems: int) -> Peer:
+    """Collective: this rank's peer group of the fused row all-reduce (CUDA IPC handles exchanged via NCCL)."""
+    h = ctypes.c_void_p()
+    call("bdlora_peer_create", comm.handle, int(max_elems), ctypes.byref(h))
+    return Peer(h.value, comm.rank, comm.nranks, comm.device)
+
+
+def bdlora_peer_create_local(nranks: int, max_elems: int, device: int = 0) -> List[Peer]:
+    """nranks emulated peer groups on one device (tests): element r is rank r's group."""
+    arr = (ctypes.c_void_p * nranks)()
+    call("bdlora_peer_create_local", int(nranks), int(device), int(max_elems), arr)
+    return [Peer(arr[r], r, nranks, device) for r in range(nranks)]
+
+
+def bdlora_peer_error(peer: Peer) -> int:
+    e = ctypes.c_int32()
+    call("bdlora_peer_error", peer.handle, ctypes.byref(e))
+    return e.value
+
+
+def bdlora_row_partial_push(pool: Pool, peer: Peer, X, W, ids, ws, stream=None) -> None:
+    torch = _torch()
+    dev = pool.tdevice
+    _need(X, "X", dtype=torch.bfloat16, device=dev)
+    T = X.shape[0]
+    _need(X, "X", shape=(T, pool.k_loc))
+    _need(W, "W", dtype=torch.bfloat16, device=dev, shape=(pool.m_loc, pool.k_loc))
+    _need(ids, "ids", dtype=torch.int32, device=dev, shape=(T,))
+    _need(ws, "workspace", dtype=torch.uint8, device=dev)
+    call("bdlora_row_partial_push", pool.handle, peer.handle, _ptr(X), T, _ptr(W), _ptr(ids), _ptr(ws), ws.numel(),
+         _stream(stream))
+
+
+def bdlora_peer_reduce(peer: Peer, Y, stream=None) -> None:
+    torch = _torch()
+    _need(Y, "Y", dtype=torch.bfloat16)
+    call("bdlora_peer_reduce", peer.handle, _ptr(Y), Y.shape[0], Y.shape[1], _stream(stream))
+
+
+def bdlora_row_forward_fused(pool: Pool, peer: Peer, X, W, ids, Y, ws, stream=None) -> None:
+    """Row layer with the base all-reduce fused into the GEMM over peer memory (include/bdlora.h)."""
+    T = _check_fwd(pool, X, W, ids, Y, ws, pool.k_loc, pool.m_loc)
+    call("bdlora_row_forward_fused", pool.handle, peer.handle, _ptr(X), T, _ptr(W), _ptr(ids), _ptr(Y), _ptr(ws),
          ws.numel(), _stream(stream))
 
 

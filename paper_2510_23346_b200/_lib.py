@@ -50,6 +50,13 @@ SIGNATURES = {
     "bdlora_pool_geometry": (c_int, [c_vp, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "bdlora_workspace_bytes": (c_int, [c_vp, c_i64, ctypes.POINTER(c_size)]),
     "bdlora_workspace_init": (c_int, [c_vp, c_vp, c_size, c_vp]),
+    "bdlora_peer_create": (c_int, [c_vp, c_i64, ctypes.POINTER(c_vp)]),
+    "bdlora_peer_create_local": (c_int, [c_int, c_int, c_i64, ctypes.POINTER(c_vp)]),
+    "bdlora_peer_destroy": (c_int, [c_vp]),
+    "bdlora_peer_error": (c_int, [c_vp, ctypes.POINTER(c_i32)]),
+    "bdlora_row_partial_push": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "bdlora_peer_reduce": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp]),
+    "bdlora_row_forward_fused": (c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "bdlora_last_launch_info": (c_int, [ctypes.POINTER(c_i32)]),
     "bdlora_build_segments": (c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "bdlora_column_forward": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),

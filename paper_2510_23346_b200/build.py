@@ -31,14 +31,15 @@ def nccl_dir() -> str:
 
 def sources():
     """Translation units, built in parallel into objects under build/ and linked into one .so."""
-    return [os.path.join(CSRC, "runtime.cu"), os.path.join(CSRC, "decode.cu")]
+    return [os.path.join(CSRC, "runtime.cu"), os.path.join(CSRC, "decode.cu"), os.path.join(CSRC, "peer.cu")]
 
 
 # private headers of each translation unit (a change rebuilds only the units that include them)
 _TU_DEPS = {
     "runtime.cu": ["runtime.cu", "common.cuh", "ptx.cuh", "kernels_core.cuh", "kernels_umma.cuh", "kernels_route.cuh",
-                   "decode.h", "../../include/bdlora.h"],
-    "decode.cu": ["decode.cu", "decode.h", "kernels_decode.cuh", "common.cuh", "ptx.cuh"],
+                   "decode.h", "peer.h", "../../include/bdlora.h"],
+    "decode.cu": ["decode.cu", "decode.h", "kernels_decode.cuh", "common.cuh", "ptx.cuh", "peer.h"],
+    "peer.cu": ["peer.cu", "peer.h"],
 }
 
 

@@ -214,6 +214,8 @@ int dec_launch(const DecLaunch& a) {
   p.cnt = (int*)a.cnt;
   p.lora = a.lora;
   p.pdl = a.pdl;
+  p.push = a.push;
+  p.peer = a.peer;
   p.trace = g_dec_trace;
   CUtensorMap tmW, tmX;
   if (!encode(&tmW, a.W, p.K, p.M, kDecBM)) return 3;
@@ -225,6 +227,7 @@ int dec_launch(const DecLaunch& a) {
   const int smax = deep ? 8 : p.cluster > 1 ? 4 : 5;
   const int stages = std::min(smax, std::max(2, env_int("BDLORA_DEC_STAGES", smax)));
   p.nstages = stages;
+  if (a.grid_out) *a.grid_out = p.grid;
   g_dec_last[0] = 3;
   g_dec_last[1] = kDecBN;
   g_dec_last[2] = p.grid;

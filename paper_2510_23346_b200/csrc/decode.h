@@ -6,6 +6,7 @@
 #include <stddef.h>
 
 #include "common.cuh"
+#include "peer.h"
 
 namespace bdl {
 
@@ -24,8 +25,11 @@ struct DecLaunch {
   int num_sms;
   cudaStream_t stream;
   int pdl;
-  int lora;                   // 1 K-local, 2 v precomputed
+  int lora;                   // 1 K-local, 2 v precomputed (per-output gather), 3 v precomputed (B rows staged)
   const CUtensorMap* amap;    // the pool arena as [rows, K] bf16 with 16-row boxes (tensor-core K-local shrink), or null
+  int push;                   // 1: fused row all-reduce -- fp32 partial pushed to every rank of `peer` (not Y)
+  PeerDev peer;
+  int* grid_out;              // optional: the launched grid (the reduce kernel's expected arrivals / rank)
 };
 
 constexpr int kDecMaxT = 16;

@@ -27,6 +27,7 @@
 // 2 = v precomputed (S-LoRA, after its all-gather / all-reduce): the tile's finisher adds s v B[a].
 #pragma once
 #include "common.cuh"
+#include "peer.h"
 #include "ptx.cuh"
 
 namespace bdl {
@@ -50,13 +51,26 @@ struct DecParams {
   __nv_bfloat16* Y;
   float* part;        // [grid][2][128][16] fp32 split-tile partials (slot 0: a CTA's first segment, 1: its last)
   int* cnt;           // [kDecMaxGrid] arrival counters of split tiles, zero between launches
-  int lora;           // 0 none, 1 K-local, 2 v precomputed
+  int lora;           // 0 none, 1 K-local, 2 v precomputed (per-output gather), 3 v precomputed (B staged)
   int pdl;
   int nstages;
   int cluster;        // > 1: the tile's contributors are one thread-block cluster (DSMEM reduce, CL instantiation)
   int tc_shrink;      // CL: the K-local shrink may run on the tensor cores (tmA = the arena's 16-row A boxes)
   long long* trace;   // optional per-CTA %globaltimer stamps (32 per CTA)
+  int push;           // 1: row partial pushed (fp32) into every rank's receive slot instead of stored to Y
+  PeerDev peer;       // push == 1: the peer group (peer.h)
 };
+
+// One output element: y_t[n] rounded once to bf16 into Y, or -- fused row all-reduce -- the fp32 partial
+// written into slot [parity][this rank] of every rank's receive buffer (NVLink stores for the peers).
+__device__ __forceinline__ void dec_out(const DecParams& p, int par, int t, int n, float y) {
+  if (p.push) {
+    const size_t off = ((size_t)(par * p.peer.nranks + p.peer.rank)) * p.peer.slot + (size_t)t * p.M + n;
+    for (int r = 0; r < p.peer.nranks; ++r) __stcg(p.peer.recv[r] + off, y);
+  } else {
+    p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y);
+  }
+}
 
 template <int S, bool CL>
 struct DecSmem {
@@ -151,6 +165,17 @@ __device__ __noinline__ void dec_stage_B(const DecParams* pp, int tile, int row,
 __device__ __forceinline__ float dec_dot(const float* vs, const uint16_t* sb, int rs) {
   float s0 = 0.f;
   for (int k = 0; k < rs; ++k) s0 = fmaf(vs[k], bf16_bits_to_f32(sb[k * kDecBM]), s0);
+  return s0;
+}
+
+// lora == 3: s v[t][j] . B[:, n] over the expand rank re, v [C][T][J][Rc] fp32 (rank row k = c * re/C + kk)
+__device__ __forceinline__ float dec_vdot(const DecParams& p, int t, int j, const uint16_t* sb, int re) {
+  const int C = p.g.C, rc = re / C;
+  float s0 = 0.f;
+  for (int c = 0; c < C; ++c) {
+    const float* vv = p.v + ((size_t)(c * p.T + t) * p.g.J + j) * p.g.Rc;
+    for (int kk = 0; kk < rc; ++kk) s0 = fmaf(__ldg(vv + kk), bf16_bits_to_f32(sb[(c * rc + kk) * kDecBM]), s0);
+  }
   return s0;
 }
 
@@ -351,7 +376,9 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
     // written by the kernel immediately preceding a forward (include/bdlora.h, bdlora_set_pdl), so the LoRA
     // metadata, the first tile's B rows and an L2 prefetch of the first segment's A rows all overlap the
     // preceding kernel's tail; after the wait only X (L2-resident) is still to be read.
-    if (p.lora == 1) {
+    // lora == 3 (v precomputed, staged): the same groups, with the EXPAND rank re as the rank rows
+    const bool lgrp = p.lora == 1 || p.lora == 3;
+    if (lgrp) {
       if (we == 0) {
         // lane t < T holds token t's id; leaders (first token of each id) in token order define the groups
         const int id = (lane < T) ? __ldg(p.ids + lane) : -1;
@@ -375,7 +402,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
         int rs = 0;
         if (lead) {
           const SlotEntry e = p.tab[id];
-          rs = min(e.rs, kDecLoraRows);
+          rs = min(p.lora == 3 ? e.re : e.rs, kDecLoraRows);
           s_gad[gidx] = id;
           s_gsc[gidx] = e.scale;
 #pragma unroll
@@ -414,17 +441,19 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       }
       ptx::named_bar_sync(1, 128);
     }
-    const int ngroups = (p.lora == 1) ? mi[96] : 0;
-    const int lrows = (p.lora == 1) ? mi[97] : 0;
+    const int ngroups = lgrp ? mi[96] : 0;
+    const int lrows = lgrp ? mi[97] : 0;
     int cur_tile = -1;
     auto stage_B = [&](int tile) {
       dec_stage_B(&p, tile, row, lrows, ngroups, s_gq0, s_goff, s_B);
       cur_tile = tile;
     };
-    if (p.lora == 1 && ngroups > 0 && u_lo < u_hi) {
-      const int tile = u_lo / p.k_blocks, kb0 = u_lo - tile * p.k_blocks;
+    if (lgrp && ngroups > 0 && u_lo < u_hi) {
+      const int tile = u_lo / p.k_blocks;
+      int kb0 = u_lo - tile * p.k_blocks;
       const int kb1 = min(p.k_blocks, kb0 + (u_hi - u_lo));
       stage_B(tile);
+      if (p.lora == 3) kb0 = kb1;  // no A prefetch: v comes from the preceding kernel
       // L2 prefetch of the first segment's A rows (one bulk prefetch per row and slice)
       const int n0 = tile * kDecBM;
       const int jlo = dec_slice_of(p.g, n0), jhi = dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
@@ -438,6 +467,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       }
     }
     if (p.pdl) ptx::pdl_wait();  // X (and v) of the preceding kernel are visible; orders our Y writes
+    const int par = p.push ? *p.peer.parity : 0;
     long long vs_key = -1;       // (slice range, K range) whose v_seg s_vs holds
 
     int acc = 0;
@@ -569,6 +599,24 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
           }
         }
       }
+      if (p.lora == 3 && ngroups > 0) {
+        // ---- v precomputed (S-LoRA after its collective), B rows staged before the wait: the tile's LoRA
+        // term, added by ONE contributor (whole tile; cluster rank 0; the split tile's first contributor)
+        if (tile != cur_tile) stage_B(tile);
+        const bool mine = whole || (CL ? ptx::cluster_ctarank() == 0
+                                       : cta == dec_cta_of((long long)tile * p.k_blocks, UNITS, GRID));
+        if (mine) {
+          if (T == 1) {
+            const int g = s_grp[0];
+            if (g >= 0) lr[0] = dec_vdot(p, 0, jn, s_B + s_gq0[g] * kDecBM + row, s_grs[g]);
+          } else {
+#pragma unroll
+            for (int t = 0; t < kDecBN; ++t)
+              if (t < T && s_grp[t] >= 0)
+                lr[t] = dec_vdot(p, t, jn, s_B + s_gq0[s_grp[t]] * kDecBM + row, s_grs[s_grp[t]]);
+          }
+        }
+      }
       if (u == u_lo && etid == 0) DEC_TRACE(3);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
@@ -648,7 +696,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (qd * 4 + i < T) p.Y[(size_t)(qd * 4 + i) * p.M + nn] = __float2bfloat16_rn(yv[i]);
+              if (qd * 4 + i < T) dec_out(p, par, qd * 4 + i, nn, yv[i]);
           }
         }
       } else if (whole) {
@@ -662,7 +710,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
         if (n < p.M) {
 #pragma unroll
           for (int t = 0; t < kDecBN; ++t)
-            if (t < T) p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(__uint_as_float(r[t]) + lr[t]);
+            if (t < T) dec_out(p, par, t, n, __uint_as_float(r[t]) + lr[t]);
         }
       } else {
         // split tile: this CTA's fp32 partial (its K range, with its K-local LoRA share) -> its slot,
@@ -722,7 +770,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
             }
 #pragma unroll
             for (int t = 0; t < kDecBN; ++t)
-              if (t < T) p.Y[(size_t)t * p.M + n] = __float2bfloat16_rn(y[t]);
+              if (t < T) dec_out(p, par, t, n, y[t]);
           }
           if (etid == 0) p.cnt[c_first] = 0;  // re-arm for the next launch
         }
@@ -733,6 +781,15 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       u += kb1 - kb0;
     }
     if (etid == 0) DEC_TRACE(7);
+    if (p.push) {
+      // every CTA signals every rank once, after all of its pushes: barrier, then a system-scope release
+      ptx::named_bar_sync(1, 128);
+      if (etid == 0) {
+        __threadfence_system();
+        for (int r2 = 0; r2 < p.peer.nranks; ++r2)
+          asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p.peer.cnt[r2] + par) : "memory");
+      }
+    }
   }
   if (warp == 0 && lane == 0) DEC_TRACE(8);  // producer done issuing
   if (CL && warp < 2) {  // the epilogue's cluster barriers count every thread of the CTA

@@ -18,6 +18,7 @@
 #include "decode.h"
 #include "kernels_core.cuh"
 #include "kernels_umma.cuh"
+#include "peer.h"
 
 using bdl::Geom;
 using bdl::SlotEntry;
@@ -80,6 +81,20 @@ struct bdlora_comm {
   ncclComm_t nccl = nullptr;
   int nranks = 1, rank = 0, dev = 0;
   int64_t counts[6] = {0, 0, 0, 0, 0, 0};
+};
+
+// Peer group of the fused row all-reduce (include/bdlora.h, kernels_decode.cuh push mode + peer.cu).
+struct bdlora_peer {
+  int dev = 0, rank = 0, nranks = 1;
+  long long slot = 0;            // fp32 elements per (parity, source rank) slot
+  float* recv = nullptr;         // own receive buffer [2][nranks][slot]
+  int* ctrl = nullptr;           // own control block: [0..1] arrival counters (unsigned), [2] parity, [3] done, [4] err
+  std::vector<void*> opened;     // IPC-opened peer allocations (closed on destroy)
+  std::vector<void*> owned;      // allocations to free on destroy
+  float** d_recv = nullptr;      // device array [nranks]: every rank's receive buffer in this address space
+  unsigned** d_cnt = nullptr;    // device array [nranks]: every rank's counters
+  bdl::PeerDev dev_view{};
+  int last_grid = 0;             // CTAs of the last push (each signals every rank once)
 };
 
 struct bdlora_pool {
@@ -226,6 +241,7 @@ int check_fwd_args(const bdlora_pool* p, const void* X, int64_t T, const void* W
 
 // ---------------------------------------------------------------------------- launches
 int g_pdl = 1;  // programmatic dependent launch chaining (bdlora_set_pdl)
+thread_local bdlora_peer* g_push = nullptr;  // set around the decode launch of bdlora_row_partial_push
 
 WsLayout ws_layout(const bdlora_pool* p, int64_t T);
 
@@ -347,6 +363,14 @@ int launch_decode(const bdlora_pool* p, const void* X, int T, const void* W, con
   a.pdl = g_pdl;
   a.lora = lora;
   a.amap = p->amap_ok ? &p->amap : nullptr;
+  a.push = 0;
+  a.peer = bdl::PeerDev{};
+  a.grid_out = nullptr;
+  if (g_push) {  // fused row all-reduce (bdlora_row_partial_push): set by the caller for this one launch
+    a.push = 1;
+    a.peer = g_push->dev_view;
+    a.grid_out = &g_push->last_grid;
+  }
   const int rc = bdl::dec_launch(a);
   if (rc < 0) return fail(BDLORA_E_CUDA, "decode kernel launch: %s", cudaGetErrorString(cudaGetLastError()));
   if (rc > 0) return -1;  // shape not handled here
@@ -367,7 +391,10 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
   const int pdl = g_pdl;
   if (T == 0) return BDLORA_OK;
   if (bdl::dec_enabled() && bdl::dec_eligible(p->g, T)) {
-    const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, 2);
+    // v precomputed: staged-B expand (mode 3) when the batch's distinct adapters fit the kernel's rank-row
+    // capacity in the worst case, else the per-output gather (mode 2)
+    const bool staged = (int64_t)std::min<int64_t>(T, p->d.capacity) * p->re_max <= bdl::kDecLoraRowsHost;
+    const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, staged ? 3 : 2);
     if (rc >= 0) return rc;
   }
   if (bdl::umma_eligible(p->g, T)) {
@@ -1103,6 +1130,211 @@ int nfs_row_forward(bdlora_pool* p, bdlora_comm* comm, const void* X, int64_t T,
     comm->counts[3] += (int64_t)n * 2;
   }
   return BDLORA_OK;
+}
+
+// ---------------------------------------------------------------------------- fused row all-reduce (8(f) row 2)
+namespace {
+
+int peer_finish_setup(bdlora_peer* q, const std::vector<float*>& recvs, const std::vector<unsigned*>& cnts) {
+  const int N = q->nranks;
+  CU_TRY(cudaMalloc(&q->d_recv, sizeof(float*) * N));
+  CU_TRY(cudaMalloc(&q->d_cnt, sizeof(unsigned*) * N));
+  CU_TRY(cudaMemcpy(q->d_recv, recvs.data(), sizeof(float*) * N, cudaMemcpyHostToDevice));
+  CU_TRY(cudaMemcpy(q->d_cnt, cnts.data(), sizeof(unsigned*) * N, cudaMemcpyHostToDevice));
+  q->dev_view.recv = q->d_recv;
+  q->dev_view.cnt = q->d_cnt;
+  q->dev_view.parity = q->ctrl + 2;
+  q->dev_view.rank = q->rank;
+  q->dev_view.nranks = N;
+  q->dev_view.slot = q->slot;
+  return BDLORA_OK;
+}
+
+int peer_alloc_own(bdlora_peer* q) {
+  const size_t bytes = sizeof(float) * 2 * (size_t)q->nranks * q->slot;
+  CU_TRY(cudaMalloc(&q->recv, bytes));
+  CU_TRY(cudaMalloc(&q->ctrl, 256));
+  CU_TRY(cudaMemset(q->ctrl, 0, 256));
+  CU_TRY(cudaMemset(q->recv, 0, bytes));
+  q->owned.push_back(q->recv);
+  q->owned.push_back(q->ctrl);
+  return BDLORA_OK;
+}
+
+int check_row_push(const bdlora_pool* p, const bdlora_peer* q, int64_t T, const char* fn) {
+  if (!q) return fail(BDLORA_E_ARG, "%s: peer is NULL", fn);
+  if (p->d.parallel != BDLORA_ROW || p->d.sharding == BDLORA_SHARD_SLORA)
+    return fail(BDLORA_E_MODE, "%s: needs a ROW pool with BD or NFS sharding", fn);
+  if (q->nranks != p->d.tp_size || q->rank != p->d.tp_rank)
+    return fail(BDLORA_E_ARG, "%s: peer (nranks=%d, rank=%d) does not match pool (tp_size=%d, tp_rank=%d)", fn,
+                q->nranks, q->rank, p->d.tp_size, p->d.tp_rank);
+  if (q->dev != p->dev) return fail(BDLORA_E_ARG, "%s: peer device %d != pool device %d", fn, q->dev, p->dev);
+  if (T > bdl::kDecMaxT || !bdl::dec_eligible(p->g, (int)T) || !decode_klocal_ok(p, (int)T))
+    return fail(BDLORA_E_CAPACITY, "%s: the fused all-reduce serves decode batches (T <= %d, K %% 64 == 0, K-local "
+                "LoRA capacity); T = %lld -- use bdlora_row_forward", fn, bdl::kDecMaxT, (long long)T);
+  if ((long long)T * p->g.M > q->slot)
+    return fail(BDLORA_E_CAPACITY, "%s: T x d_out = %lld exceeds the peer slot (%lld elements)", fn,
+                (long long)T * p->g.M, q->slot);
+  return BDLORA_OK;
+}
+
+}  // namespace
+
+int bdlora_peer_create(bdlora_comm* comm, int64_t max_elems, bdlora_peer** out) {
+  if (!comm || !out) return fail(BDLORA_E_ARG, "comm/out is NULL");
+  if (max_elems < 1 || max_elems > (1LL << 32)) return fail(BDLORA_E_ARG, "max_elems = %lld", (long long)max_elems);
+  DeviceGuard dg(comm->dev);
+  bdlora_peer* q = new bdlora_peer();
+  q->dev = comm->dev;
+  q->rank = comm->rank;
+  q->nranks = comm->nranks;
+  q->slot = max_elems;
+  int rc = peer_alloc_own(q);
+  if (rc) {
+    bdlora_peer_destroy(q);
+    return rc;
+  }
+  // exchange the CUDA IPC handles of every rank's receive buffer and control block over the communicator
+  const int N = q->nranks;
+  cudaIpcMemHandle_t mine[2];
+  if (cudaIpcGetMemHandle(&mine[0], q->recv) != cudaSuccess || cudaIpcGetMemHandle(&mine[1], q->ctrl) != cudaSuccess) {
+    bdlora_peer_destroy(q);
+    return fail(BDLORA_E_CUDA, "cudaIpcGetMemHandle failed");
+  }
+  void* dbuf = nullptr;
+  const size_t hb = sizeof(mine);
+  if (cudaMalloc(&dbuf, hb * (N + 1)) != cudaSuccess) {
+    bdlora_peer_destroy(q);
+    return fail(BDLORA_E_CUDA, "cudaMalloc (handle exchange)");
+  }
+  std::vector<uint8_t> all(hb * N);
+  cudaMemcpy((char*)dbuf + hb * N, mine, hb, cudaMemcpyHostToDevice);
+  ncclResult_t nr = ncclAllGather((char*)dbuf + hb * N, dbuf, hb, ncclUint8, comm->nccl, 0);
+  cudaError_t ce = cudaStreamSynchronize(0);
+  if (ce == cudaSuccess) ce = cudaMemcpy(all.data(), dbuf, hb * N, cudaMemcpyDeviceToHost);
+  cudaFree(dbuf);
+  if (nr != ncclSuccess || ce != cudaSuccess) {
+    bdlora_peer_destroy(q);
+    return fail(BDLORA_E_NCCL, "handle exchange: %s / %s", ncclGetErrorString(nr), cudaGetErrorString(ce));
+  }
+  std::vector<float*> recvs(N);
+  std::vector<unsigned*> cnts(N);
+  for (int r = 0; r < N; ++r) {
+    if (r == q->rank) {
+      recvs[r] = q->recv;
+      cnts[r] = (unsigned*)q->ctrl;
+      continue;
+    }
+    cudaIpcMemHandle_t h[2];
+    memcpy(h, all.data() + hb * r, hb);
+    void *pr = nullptr, *pc = nullptr;
+    if (cudaIpcOpenMemHandle(&pr, h[0], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+        cudaIpcOpenMemHandle(&pc, h[1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      bdlora_peer_destroy(q);
+      return fail(BDLORA_E_CUDA, "cudaIpcOpenMemHandle (rank %d): %s", r, cudaGetErrorString(cudaGetLastError()));
+    }
+    q->opened.push_back(pr);
+    q->opened.push_back(pc);
+    recvs[r] = (float*)pr;
+    cnts[r] = (unsigned*)pc;
+  }
+  rc = peer_finish_setup(q, recvs, cnts);
+  if (rc) {
+    bdlora_peer_destroy(q);
+    return rc;
+  }
+  *out = q;
+  return BDLORA_OK;
+}
+
+int bdlora_peer_create_local(int nranks, int cuda_device, int64_t max_elems, bdlora_peer** out) {
+  if (!out) return fail(BDLORA_E_ARG, "out is NULL");
+  if (nranks < 1 || nranks > 64) return fail(BDLORA_E_ARG, "nranks = %d", nranks);
+  if (max_elems < 1 || max_elems > (1LL << 32)) return fail(BDLORA_E_ARG, "max_elems = %lld", (long long)max_elems);
+  ST_TRY(bdlora_device_check(cuda_device));
+  DeviceGuard dg(cuda_device);
+  std::vector<bdlora_peer*> qs(nranks, nullptr);
+  std::vector<float*> recvs(nranks);
+  std::vector<unsigned*> cnts(nranks);
+  int rc = BDLORA_OK;
+  for (int r = 0; r < nranks && rc == BDLORA_OK; ++r) {
+    qs[r] = new bdlora_peer();
+    qs[r]->dev = cuda_device;
+    qs[r]->rank = r;
+    qs[r]->nranks = nranks;
+    qs[r]->slot = max_elems;
+    rc = peer_alloc_own(qs[r]);
+    if (rc == BDLORA_OK) {
+      recvs[r] = qs[r]->recv;
+      cnts[r] = (unsigned*)qs[r]->ctrl;
+    }
+  }
+  for (int r = 0; r < nranks && rc == BDLORA_OK; ++r) rc = peer_finish_setup(qs[r], recvs, cnts);
+  if (rc) {
+    for (auto* q : qs)
+      if (q) bdlora_peer_destroy(q);
+    return rc;
+  }
+  for (int r = 0; r < nranks; ++r) out[r] = qs[r];
+  return BDLORA_OK;
+}
+
+int bdlora_peer_destroy(bdlora_peer* q) {
+  if (!q) return BDLORA_OK;
+  DeviceGuard dg(q->dev);
+  cudaDeviceSynchronize();
+  for (void* pp : q->opened) cudaIpcCloseMemHandle(pp);
+  for (void* pp : q->owned) cudaFree(pp);
+  if (q->d_recv) cudaFree(q->d_recv);
+  if (q->d_cnt) cudaFree(q->d_cnt);
+  delete q;
+  return BDLORA_OK;
+}
+
+int bdlora_peer_error(const bdlora_peer* q, int32_t* err) {
+  if (!q || !err) return fail(BDLORA_E_ARG, "peer/err is NULL");
+  DeviceGuard dg(q->dev);
+  int v = 0;
+  CU_TRY(cudaMemcpy(&v, q->ctrl + 4, sizeof(int), cudaMemcpyDeviceToHost));
+  *err = v;
+  return BDLORA_OK;
+}
+
+int bdlora_row_partial_push(bdlora_pool* p, bdlora_peer* q, const void* X, int64_t T, const void* W,
+                            const int32_t* ids, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, (const void*)1, ws, ws_bytes));
+  if (T == 0) return BDLORA_OK;
+  ST_TRY(check_row_push(p, q, T, "bdlora_row_partial_push"));
+  DeviceGuard dg(p->dev);
+  g_push = q;
+  const int rc = launch_decode(p, X, (int)T, W, ids, nullptr, nullptr, ws, (cudaStream_t)stream, 1);
+  g_push = nullptr;
+  if (rc < 0) return fail(BDLORA_E_CAPACITY, "bdlora_row_partial_push: shape not served by the decode kernel");
+  return rc;
+}
+
+int bdlora_peer_reduce(bdlora_peer* q, void* Y, int64_t T, int32_t M, bdlora_stream_t stream) {
+  if (!q) return fail(BDLORA_E_ARG, "peer is NULL");
+  if (T < 0 || M < 1) return fail(BDLORA_E_ARG, "T = %lld, M = %d", (long long)T, M);
+  if (T == 0) return BDLORA_OK;
+  if (!Y) return fail(BDLORA_E_ARG, "Y is NULL");
+  if ((long long)T * M > q->slot) return fail(BDLORA_E_CAPACITY, "T x M exceeds the peer slot");
+  if (q->last_grid <= 0) return fail(BDLORA_E_ARG, "bdlora_peer_reduce: no push was issued on this peer");
+  DeviceGuard dg(q->dev);
+  const unsigned expected = (unsigned)q->nranks * (unsigned)q->last_grid;
+  if (bdl::peer_reduce_launch(q->recv, (unsigned*)q->ctrl, q->ctrl + 2, q->ctrl + 3, q->ctrl + 4, expected, q->nranks,
+                              q->slot, (__nv_bfloat16*)Y, (int)T, M, g_pdl, (cudaStream_t)stream) != 0)
+    return fail(BDLORA_E_CUDA, "peer reduce launch: %s", cudaGetErrorString(cudaGetLastError()));
+  count_launch();
+  return BDLORA_OK;
+}
+
+int bdlora_row_forward_fused(bdlora_pool* p, bdlora_peer* q, const void* X, int64_t T, const void* W,
+                             const int32_t* ids, void* Y, void* ws, size_t ws_bytes, bdlora_stream_t stream) {
+  ST_TRY(check_fwd_args(p, X, T, W, ids, Y, ws, ws_bytes));
+  if (T == 0) return BDLORA_OK;
+  ST_TRY(bdlora_row_partial_push(p, q, X, T, W, ids, ws, ws_bytes, stream));
+  return bdlora_peer_reduce(q, Y, T, p->g.M, stream);
 }
 
 // ---------------------------------------------------------------------------- S-LoRA

@@ -90,6 +90,24 @@ def test_null_arguments(lib):
     assert lib.bdlora_comm_destroy(None) == 0
 
 
+def test_peer_host_validation(lib):
+    """Fused row all-reduce peer groups: argument errors are caught on the host before any device work."""
+    import ctypes as ct
+
+    arr = (ct.c_void_p * 4)()
+    assert lib.bdlora_peer_create_local(0, 0, 1024, arr) == 1
+    assert lib.bdlora_peer_create_local(2, 0, 0, arr) == 1
+    assert lib.bdlora_peer_create_local(2, 0, 1024, None) == 1
+    assert lib.bdlora_peer_create(None, 1024, arr) == 1
+    assert lib.bdlora_peer_destroy(None) == 0
+    assert lib.bdlora_peer_reduce(None, None, 1, 1, None) == 1
+    assert lib.bdlora_row_forward_fused(None, None, None, 1, None, None, None, None, 0, None) == 1
+    assert lib.bdlora_peer_error(None, None) == 1
+    assert lib.bdlora_workspace_init(None, None, 0, None) == 1
+    info = (ct.c_int32 * 8)()
+    assert lib.bdlora_last_launch_info(info) == 0 and info[0] == -1
+
+
 def test_device_check_without_gpu(lib):
     import torch
 
