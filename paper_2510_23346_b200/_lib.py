@@ -96,7 +96,12 @@ def load() -> ctypes.CDLL:
             f"libbdlora.so not found at {LIB_PATH}: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    # BDLORA_AB_OLD_LIB=1 (same-box A/B tooling only, scripts/ab_dec.sh): an older build may lack newer entry
+    # points; they are then left unbound instead of failing the load
+    tolerant = os.environ.get("BDLORA_AB_OLD_LIB") == "1"
     for name, (res, args) in SIGNATURES.items():
+        if tolerant and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

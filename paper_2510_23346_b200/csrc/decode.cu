@@ -49,19 +49,19 @@ int env_int(const char* name, int dflt) {
   return s ? atoi(s) : dflt;
 }
 
-template <int S, bool CL>
-int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
-                  cudaStream_t st) {
+template <int S, bool CL, int LM, bool PUSH>
+int launch_one(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
+               cudaStream_t st) {
   using L = DecSmem<S, CL>;
   static bool attr[kMaxDev] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   dev = std::min(std::max(dev, 0), kMaxDev - 1);
   if (!attr[dev]) {
-    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL, LM, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024) != cudaSuccess)
       return -1;
-    if (CL && cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+    if (CL && cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL, LM, PUSH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
                   cudaSuccess)
       return -1;
     attr[dev] = true;
@@ -85,7 +85,14 @@ int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap&
     at[1].val.clusterDim.z = 1;
     cfg.numAttrs = 2;
   }
-  return cudaLaunchKernelEx(&cfg, dec_lora_gemm_kernel<S, CL>, tmW, tmX, tmA, p) == cudaSuccess ? 0 : -1;
+  return cudaLaunchKernelEx(&cfg, dec_lora_gemm_kernel<S, CL, LM, PUSH>, tmW, tmX, tmA, p) == cudaSuccess ? 0 : -1;
+}
+
+template <int S, bool CL>
+int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
+                  cudaStream_t st) {
+  if (p.lora >= 2) return launch_one<S, CL, 2, false>(p, tmW, tmX, tmA, st);
+  return p.push ? launch_one<S, CL, 1, true>(p, tmW, tmX, tmA, st) : launch_one<S, CL, 1, false>(p, tmW, tmX, tmA, st);
 }
 
 // Largest cluster size c in [2, want] such that `need` clusters of instantiation <S, true> are co-resident
@@ -105,8 +112,9 @@ int fit_cluster(int want, int need) {
   for (int c = want; c >= 2; --c) {
     int& mc = cache[dev][c];
     if (mc < 0) {
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024);
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t qc = {};
       qc.gridDim = dim3(c * need);
       qc.blockDim = dim3(kDecThreads);
@@ -118,7 +126,7 @@ int fit_cluster(int want, int need) {
       ca[0].val.clusterDim.z = 1;
       qc.attrs = ca;
       qc.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<S, true>, &qc) != cudaSuccess) {
+      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<S, true, 1, false>, &qc) != cudaSuccess) {
         cudaGetLastError();
         mc = 0;
       }

@@ -63,8 +63,9 @@ struct DecParams {
 
 // One output element: y_t[n] rounded once to bf16 into Y, or -- fused row all-reduce -- the fp32 partial
 // written into slot [parity][this rank] of every rank's receive buffer (NVLink stores for the peers).
+template <bool PUSH>
 __device__ __forceinline__ void dec_out(const DecParams& p, int par, int t, int n, float y) {
-  if (p.push) {
+  if (PUSH) {
     const size_t off = ((size_t)(par * p.peer.nranks + p.peer.rank)) * p.peer.slot + (size_t)t * p.M + n;
     for (int r = 0; r < p.peer.nranks; ++r) __stcg(p.peer.recv[r] + off, y);
   } else {
@@ -179,11 +180,14 @@ __device__ __forceinline__ float dec_vdot(const DecParams& p, int t, int j, cons
   return s0;
 }
 
-template <int S, bool CL>
+// LM: 1 = K-local LoRA (BD / NFS: lora modes 0, 1), 2 = v precomputed (S-LoRA: modes 2, 3).  PUSH: fused row
+// all-reduce output (LM == 1 only).  Separate instantiations keep each path's code and registers its own.
+template <int S, bool CL, int LM, bool PUSH>
 __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
     dec_lora_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                          const __grid_constant__ CUtensorMap tmA, const __grid_constant__ DecParams p) {
   using L = DecSmem<S, CL>;
+  static_assert(!PUSH || LM == 1, "the fused all-reduce serves the K-local (BD / NFS) path");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       // ids and the slot table are read before the dependency (bdlora_set_pdl contract).
       bool use_tc = false;
       int arow = 0;
-      if (CL && p.lora == 1 && p.tc_shrink && nu > 0) {
+      if (CL && LM == 1 && p.lora == 1 && p.tc_shrink && nu > 0) {
         int ids_r[kDecBN];
 #pragma unroll
         for (int t = 0; t < kDecBN; ++t) ids_r[t] = t < p.T ? __ldg(p.ids + t) : -1;
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
     // metadata, the first tile's B rows and an L2 prefetch of the first segment's A rows all overlap the
     // preceding kernel's tail; after the wait only X (L2-resident) is still to be read.
     // lora == 3 (v precomputed, staged): the same groups, with the EXPAND rank re as the rank rows
-    const bool lgrp = p.lora == 1 || p.lora == 3;
+    const bool lgrp = (LM == 1 && p.lora == 1) || (LM == 2 && p.lora == 3);
     if (lgrp) {
       if (we == 0) {
         // lane t < T holds token t's id; leaders (first token of each id) in token order define the groups
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
         int rs = 0;
         if (lead) {
           const SlotEntry e = p.tab[id];
-          rs = min(p.lora == 3 ? e.re : e.rs, kDecLoraRows);
+          rs = min(LM == 2 ? e.re : e.rs, kDecLoraRows);
           s_gad[gidx] = id;
           s_gsc[gidx] = e.scale;
 #pragma unroll
@@ -453,7 +457,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       int kb0 = u_lo - tile * p.k_blocks;
       const int kb1 = min(p.k_blocks, kb0 + (u_hi - u_lo));
       stage_B(tile);
-      if (p.lora == 3) kb0 = kb1;  // no A prefetch: v comes from the preceding kernel
+      if (LM == 2) kb0 = kb1;  // no A prefetch: v comes from the preceding kernel
       // L2 prefetch of the first segment's A rows (one bulk prefetch per row and slice)
       const int n0 = tile * kDecBM;
       const int jlo = dec_slice_of(p.g, n0), jhi = dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
@@ -467,7 +471,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       }
     }
     if (p.pdl) ptx::pdl_wait();  // X (and v) of the preceding kernel are visible; orders our Y writes
-    const int par = p.push ? *p.peer.parity : 0;
+    const int par = PUSH ? *p.peer.parity : 0;
     long long vs_key = -1;       // (slice range, K range) whose v_seg s_vs holds
 
     int acc = 0;
@@ -485,9 +489,9 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
 #pragma unroll
       for (int i = 0; i < kDecBN; ++i) lr[i] = 0.f;
       // tensor-core K-local shrink taken by the producer (same rule): v_seg arrives in TMEM with the accumulator
-      const bool tc = CL && p.tc_shrink && p.lora == 1 && ngroups == 1 && s_grs[0] <= 16 &&
+      const bool tc = CL && LM == 1 && p.tc_shrink && p.lora == 1 && ngroups == 1 && s_grs[0] <= 16 &&
                       jlo == dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
-      if (p.lora == 1 && ngroups > 0 && !tc) {
+      if (LM == 1 && p.lora == 1 && ngroups > 0 && !tc) {
         // ---- K-local shrink of this segment: v_seg[t][j][k] = s_a sum_{d in seg} X[t][d] A_{a,j}[k][d] -----
         // Thread per 16-byte chunk of the K range, 8 rank rows x 4 tokens per pass: 12 independent loads in
         // flight per chunk (the A rows are L2-resident, X was just written by the preceding kernel), then a
@@ -599,7 +603,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
           }
         }
       }
-      if (p.lora == 3 && ngroups > 0) {
+      if (LM == 2 && p.lora == 3 && ngroups > 0) {
         // ---- v precomputed (S-LoRA after its collective), B rows staged before the wait: the tile's LoRA
         // term, added by ONE contributor (whole tile; cluster rank 0; the split tile's first contributor)
         if (tile != cur_tile) stage_B(tile);
@@ -687,7 +691,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
           const int nn = n0 + r_lo + r2;
           if (nn < p.M) {
             float yv[4] = {y.x, y.y, y.z, y.w};
-            if (p.lora == 2) {
+            if (LM == 2 && p.lora == 2) {
               float lrv[kDecBN];
               dec_vmode_lr(&p, nn, lrv);
 #pragma unroll
@@ -696,11 +700,11 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              if (qd * 4 + i < T) dec_out(p, par, qd * 4 + i, nn, yv[i]);
+              if (qd * 4 + i < T) dec_out<PUSH>(p, par, qd * 4 + i, nn, yv[i]);
           }
         }
       } else if (whole) {
-        if (p.lora == 2 && n < p.M) {
+        if (LM == 2 && p.lora == 2 && n < p.M) {
           float lrv[kDecBN];
           dec_vmode_lr(&p, n, lrv);
 #pragma unroll
@@ -710,7 +714,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
         if (n < p.M) {
 #pragma unroll
           for (int t = 0; t < kDecBN; ++t)
-            if (t < T) dec_out(p, par, t, n, __uint_as_float(r[t]) + lr[t]);
+            if (t < T) dec_out<PUSH>(p, par, t, n, __uint_as_float(r[t]) + lr[t]);
         }
       } else {
         // split tile: this CTA's fp32 partial (its K range, with its K-local LoRA share) -> its slot,
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
             }
           }
           if (n < p.M) {
-            if (p.lora == 2) {
+            if (LM == 2 && p.lora == 2) {
               float lrv[kDecBN];
               dec_vmode_lr(&p, n, lrv);
 #pragma unroll
@@ -770,7 +774,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
             }
 #pragma unroll
             for (int t = 0; t < kDecBN; ++t)
-              if (t < T) dec_out(p, par, t, n, y[t]);
+              if (t < T) dec_out<PUSH>(p, par, t, n, y[t]);
           }
           if (etid == 0) p.cnt[c_first] = 0;  // re-arm for the next launch
         }
@@ -781,7 +785,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       u += kb1 - kb0;
     }
     if (etid == 0) DEC_TRACE(7);
-    if (p.push) {
+    if (PUSH) {
       // every CTA signals every rank once, after all of its pushes: barrier, then a system-scope release
       ptx::named_bar_sync(1, 128);
       if (etid == 0) {
