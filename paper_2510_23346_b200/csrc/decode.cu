@@ -49,19 +49,19 @@ int env_int(const char* name, int dflt) {
   return s ? atoi(s) : dflt;
 }
 
-template <int S, bool CL, int LM, bool PUSH>
+template <int S, bool CL, int LM, bool PUSH, int BN>
 int launch_one(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
                cudaStream_t st) {
-  using L = DecSmem<S, CL>;
+  using L = DecSmem<S, CL, BN>;
   static bool attr[kMaxDev] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   dev = std::min(std::max(dev, 0), kMaxDev - 1);
   if (!attr[dev]) {
-    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL, LM, PUSH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL, LM, PUSH, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024) != cudaSuccess)
       return -1;
-    if (CL && cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL, LM, PUSH>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+    if (CL && cudaFuncSetAttribute(dec_lora_gemm_kernel<S, CL, LM, PUSH, BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
                   cudaSuccess)
       return -1;
     attr[dev] = true;
@@ -85,19 +85,28 @@ int launch_one(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tm
     at[1].val.clusterDim.z = 1;
     cfg.numAttrs = 2;
   }
-  return cudaLaunchKernelEx(&cfg, dec_lora_gemm_kernel<S, CL, LM, PUSH>, tmW, tmX, tmA, p) == cudaSuccess ? 0 : -1;
+  return cudaLaunchKernelEx(&cfg, dec_lora_gemm_kernel<S, CL, LM, PUSH, BN>, tmW, tmX, tmA, p) == cudaSuccess ? 0 : -1;
 }
 
 template <int S, bool CL>
 int launch_stages(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
                   cudaStream_t st) {
-  if (p.lora >= 2) return launch_one<S, CL, 2, false>(p, tmW, tmX, tmA, st);
-  return p.push ? launch_one<S, CL, 1, true>(p, tmW, tmX, tmA, st) : launch_one<S, CL, 1, false>(p, tmW, tmX, tmA, st);
+  if (p.lora >= 2) return launch_one<S, CL, 2, false, 16>(p, tmW, tmX, tmA, st);
+  return p.push ? launch_one<S, CL, 1, true, 16>(p, tmW, tmX, tmA, st)
+                : launch_one<S, CL, 1, false, 16>(p, tmW, tmX, tmA, st);
+}
+
+// 17..64 tokens (one adapter per pool): BN = 64 token tiles, 6-stage ring, one CTA per SM
+template <bool CL>
+int launch_bn64(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
+                cudaStream_t st) {
+  if (p.lora >= 2) return launch_one<6, CL, 2, false, 64>(p, tmW, tmX, tmA, st);
+  return launch_one<6, CL, 1, false, 64>(p, tmW, tmX, tmA, st);
 }
 
 // Largest cluster size c in [2, want] such that `need` clusters of instantiation <S, true> are co-resident
 // (one wave: every tile's contributors run at once), cached per (device, S, size); 1 if none.
-template <int S>
+template <int S, int BN = 16>
 int fit_cluster(int want, int need) {
   static int cache[kMaxDev][kDecMaxCluster + 1];
   static bool init = false;
@@ -112,13 +121,13 @@ int fit_cluster(int want, int need) {
   for (int c = want; c >= 2; --c) {
     int& mc = cache[dev][c];
     if (mc < 0) {
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            227 * 1024);
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false, BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t qc = {};
       qc.gridDim = dim3(c * need);
       qc.blockDim = dim3(kDecThreads);
-      qc.dynamicSmemBytes = DecSmem<S, true>::kBytes;
+      qc.dynamicSmemBytes = DecSmem<S, true, BN>::kBytes;
       cudaLaunchAttribute ca[1];
       ca[0].id = cudaLaunchAttributeClusterDimension;
       ca[0].val.clusterDim.x = c;
@@ -126,7 +135,7 @@ int fit_cluster(int want, int need) {
       ca[0].val.clusterDim.z = 1;
       qc.attrs = ca;
       qc.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<S, true, 1, false>, &qc) != cudaSuccess) {
+      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<S, true, 1, false, BN>, &qc) != cudaSuccess) {
         cudaGetLastError();
         mc = 0;
       }
@@ -139,7 +148,10 @@ int fit_cluster(int want, int need) {
 }  // namespace
 
 size_t dec_counter_bytes() { return sizeof(int) * kDecMaxGrid; }
-size_t dec_scratch_bytes(int num_sms) { return (size_t)std::min(num_sms, kDecMaxGrid) * 2 * kDecBN * kDecBM * 4; }
+size_t dec_scratch_bytes(int num_sms, int T) {
+  const int bn = T <= 16 ? 16 : 64;
+  return (size_t)std::min(num_sms, kDecMaxGrid) * 2 * bn * kDecBM * 4;
+}
 bool dec_eligible(const Geom& g, int T) { return T >= 1 && T <= kDecMaxT && g.K % kDecBK == 0 && g.K >= kDecBK; }
 bool dec_enabled() {
   static int v = -1;
@@ -169,6 +181,9 @@ int dec_launch(const DecLaunch& a) {
   // projections.  tiles > #SM: stream-K over a grid that divides the tile count when such a grid keeps
   // >= 70% of the SMs busy (whole tiles per CTA, no split tiles), else over every SM.
   const int tiles = p.m_tiles;
+  const bool bn64 = a.T > 16;  // 17..64 tokens: BN = 64 token tile (the caller guarantees one adapter per pool)
+  const int BNh = bn64 ? 64 : 16;
+  if (bn64 && a.push) return 1;
   long long grid;
   const int min_kb = std::max(1, env_int("BDLORA_DEC_MINKB", 1));
   p.cluster = 1;
@@ -184,11 +199,15 @@ int dec_launch(const DecLaunch& a) {
     if (s >= 2 && cl_max >= 2) {
       const int want = std::min(s, cl_max);
       int c = 1;
-      if (deep_kb > 0 && p.k_blocks / want >= deep_kb) {
-        c = fit_cluster<8>(want, tiles);
-        deep = c >= 2;
+      if (bn64) {
+        c = fit_cluster<6, 64>(want, tiles);
+      } else {
+        if (deep_kb > 0 && p.k_blocks / want >= deep_kb) {
+          c = fit_cluster<8>(want, tiles);
+          deep = c >= 2;
+        }
+        if (c < 2) c = fit_cluster<4>(want, tiles);
       }
-      if (c < 2) c = fit_cluster<4>(want, tiles);
       if (c >= 2) {
         s = c;
         p.cluster = c;
@@ -227,17 +246,17 @@ int dec_launch(const DecLaunch& a) {
   p.trace = g_dec_trace;
   CUtensorMap tmW, tmX;
   if (!encode(&tmW, a.W, p.K, p.M, kDecBM)) return 3;
-  if (!encode(&tmX, a.X, p.K, p.T, kDecBN)) return 3;
+  if (!encode(&tmX, a.X, p.K, p.T, BNh)) return 3;
   // Long weight streams (>= 16 k-blocks = 256 KB per CTA, e.g. TP1 / TP2 projections) take a deep 8-stage ring (one CTA
   // per SM: the PDL overlap with the next projection matters little next to a 30+ us stream); the rest keep
   // <= 113 KB so two CTAs share an SM across projection boundaries.
   if (tiles > sms) deep = deep_kb > 0 && units / p.grid >= deep_kb;
-  const int smax = deep ? 8 : p.cluster > 1 ? 4 : 5;
+  const int smax = bn64 ? 6 : deep ? 8 : p.cluster > 1 ? 4 : 5;
   const int stages = std::min(smax, std::max(2, env_int("BDLORA_DEC_STAGES", smax)));
   p.nstages = stages;
   if (a.grid_out) *a.grid_out = p.grid;
   g_dec_last[0] = 3;
-  g_dec_last[1] = kDecBN;
+  g_dec_last[1] = BNh;
   g_dec_last[2] = p.grid;
   g_dec_last[3] = p.cluster;
   g_dec_last[4] = stages;
@@ -247,6 +266,7 @@ int dec_launch(const DecLaunch& a) {
   // the arena's A-row map when the pool has one (else a dummy: the tensor-core shrink is then off)
   p.tc_shrink = (a.amap != nullptr && env_int("BDLORA_DEC_TC_SHRINK", 1) != 0) ? 1 : 0;
   const CUtensorMap& tmA = a.amap ? *a.amap : tmX;
+  if (bn64) return p.cluster > 1 ? launch_bn64<true>(p, tmW, tmX, tmA, a.stream) : launch_bn64<false>(p, tmW, tmX, tmA, a.stream);
   if (p.cluster > 1)
     return deep ? launch_stages<8, true>(p, tmW, tmX, tmA, a.stream) : launch_stages<4, true>(p, tmW, tmX, tmA, a.stream);
   return deep ? launch_stages<8, false>(p, tmW, tmX, tmA, a.stream) : launch_stages<5, false>(p, tmW, tmX, tmA, a.stream);

@@ -13,7 +13,7 @@ namespace bdl {
 struct DecLaunch {
   Geom g;
   const __nv_bfloat16* X;
-  int T;                      // 1..16
+  int T;                      // 1..64 (17..64: the pool holds one adapter -- the caller checks)
   const __nv_bfloat16* W;     // W^T [M, K] bf16, K-major
   const int* ids;
   const SlotEntry* tab;
@@ -32,11 +32,12 @@ struct DecLaunch {
   int* grid_out;              // optional: the launched grid (the reduce kernel's expected arrivals / rank)
 };
 
-constexpr int kDecMaxT = 16;
+constexpr int kDecMaxT = 64;      // BN = 16 tiles up to 16 tokens, BN = 64 tiles (one-adapter pools) up to 64
+constexpr int kDecMaxPushT = 16;  // the fused row all-reduce serves BN = 16 decode batches
 constexpr int kDecLoraRowsHost = 32;  // == kDecLoraRows: K-local capacity (sum of the batch's distinct local ranks)
 
 size_t dec_counter_bytes();
-size_t dec_scratch_bytes(int num_sms);
+size_t dec_scratch_bytes(int num_sms, int T);
 bool dec_eligible(const Geom& g, int T);
 bool dec_enabled();                        // BDLORA_DECODE=0 selects the older single-kernel forward
 // Returns 0 on launch, non-zero if the shape is not handled (caller falls back), negative on a CUDA error.

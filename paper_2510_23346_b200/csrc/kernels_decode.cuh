@@ -73,10 +73,10 @@ __device__ __forceinline__ void dec_out(const DecParams& p, int par, int t, int 
   }
 }
 
-template <int S, bool CL>
+template <int S, bool CL, int BN = 16>
 struct DecSmem {
   static constexpr int kW = kDecBM * kDecBK * 2;  // 16 KB weight tile
-  static constexpr int kX = kDecBN * kDecBK * 2;  // 2 KB token tile
+  static constexpr int kX = BN * kDecBK * 2;      // token tile (2 KB at BN = 16)
   // CL: a 16-row box of the batch's adapter A rows per stage (tensor-core K-local shrink).  The ring sits
   // FIRST: the shrink MMA's operand is 128 rows (M = 128), rows 16..127 -- ignored TMEM lanes -- read the
   // next 14 KB of this CTA's own shared memory (following boxes and the weight ring), never past it
@@ -88,16 +88,20 @@ struct DecSmem {
   // misc ints: [0,16) ids  [16,32) group of token  [32,48) group adapter  [48,64) group rs  [64,80) group row
   // offset q0  [80,96) member masks  [96] n_groups  [97] rows total ; floats [128,144) group scale ;
   // long long [160 + 2*(g*3 + j)) group A / B offsets per slice (as int pairs)
-  static constexpr int kMiscBytes = 3584;
-  static constexpr int kVsOff = kMiscOff + kMiscBytes;          // v_seg [16 tokens][3 slices][32] fp32
-  static constexpr int kVsBytes = kDecBN * 3 * kDecLoraRows * 4;
+  // ... [960, 1024) group of each of up to 64 tokens
+  static constexpr int kMiscBytes = 4096;
+  // v_seg: BN = 16: [16 tokens][3 slices][32] fp32; BN = 64 (one adapter, one slice per tile): [64][32]
+  static constexpr int kVsTok = BN == 16 ? 3 * kDecLoraRows : kDecLoraRows;
+  static constexpr int kVsOff = kMiscOff + kMiscBytes;
+  static constexpr int kVsBytes = BN * kVsTok * 4;
   static constexpr int kBOff = kVsOff + kVsBytes;               // B rows [32][128] bf16 of the tile's columns
   static constexpr int kBBytes = kDecLoraRows * kDecBM * 2;
   // cluster split-K: [s][ceil(128/s)][16] fp32 partial slots the peers push into (<= (128 + s) x 16 floats)
   static constexpr int kSlotOff = kBOff + kBBytes;
-  static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * kDecBN * 4 : 0;
+  static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * BN * 4 : 0;
   static constexpr int kBytes = kSlotOff + kSlotBytes + 1024;   // + 1024-B alignment slack
-  static constexpr int kTmemCols = CL ? 64 : 32;                // [acc 0 | acc 1 | v_seg (CL)]
+  static constexpr int kVCol = 2 * BN;                          // TMEM: [acc 0 | acc 1 | v_seg (CL)]
+  static constexpr int kTmemCols = BN == 16 ? (CL ? 64 : 32) : 256;
   static_assert(S > 5 || kBytes <= 113 * 1024, "two CTAs per SM");
   static_assert(kBytes <= 227 * 1024, "shared memory per CTA");
 };
@@ -126,11 +130,12 @@ __device__ __forceinline__ int dec_slice_of(const Geom& g, int n) {
 // lora == 2 (v precomputed): lr[t] = s_a v[t] . B_a[:, n] for every token of the batch (matmul_4 / _6 after
 // S-LoRA's collective).  Out of line: it runs once per output element on the S-LoRA path only, and keeping
 // it out of the kernel body keeps the decode kernel's executed footprint small.
-__device__ __noinline__ void dec_vmode_lr(const DecParams* pp, int n, float* lr) {
+__device__ __noinline__ void dec_vmode_lr(const DecParams* pp, int n, int t0, int cnt, float* lr) {
   const DecParams& p = *pp;
-  for (int t = 0; t < p.T; ++t) {
+  for (int i = 0; i < cnt; ++i) {
+    const int t = t0 + i;
     const int a = __ldg(p.ids + t);
-    lr[t] = (a >= 0) ? lora_expand_term(t, n, a, p.tab, p.arena, p.g, p.v, p.T) : 0.f;
+    lr[i] = (a >= 0) ? lora_expand_term(t, n, a, p.tab, p.arena, p.g, p.v, p.T) : 0.f;
   }
 }
 
@@ -182,11 +187,12 @@ __device__ __forceinline__ float dec_vdot(const DecParams& p, int t, int j, cons
 
 // LM: 1 = K-local LoRA (BD / NFS: lora modes 0, 1), 2 = v precomputed (S-LoRA: modes 2, 3).  PUSH: fused row
 // all-reduce output (LM == 1 only).  Separate instantiations keep each path's code and registers its own.
-template <int S, bool CL, int LM, bool PUSH>
-__global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
+template <int S, bool CL, int LM, bool PUSH, int BN = 16>
+__global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
     dec_lora_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                          const __grid_constant__ CUtensorMap tmA, const __grid_constant__ DecParams p) {
-  using L = DecSmem<S, CL>;
+  using L = DecSmem<S, CL, BN>;
+  static_assert(BN == 16 || BN == 64, "token tile");
   static_assert(!PUSH || LM == 1, "the fused all-reduce serves the K-local (BD / NFS) path");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -201,7 +207,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
   int* s_last = (int*)(tmem_holder + 1);
   int* mi = (int*)(smem + L::kMiscOff);
   int* s_ids = mi;
-  int* s_grp = mi + 16;
+  int* s_grp = mi + 960;  // [64]
   int* s_gad = mi + 32;
   int* s_grs = mi + 48;
   int* s_gq0 = mi + 64;
@@ -276,17 +282,16 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       bool use_tc = false;
       int arow = 0;
       if (CL && LM == 1 && p.lora == 1 && p.tc_shrink && nu > 0) {
-        int ids_r[kDecBN];
-#pragma unroll
-        for (int t = 0; t < kDecBN; ++t) ids_r[t] = t < p.T ? __ldg(p.ids + t) : -1;
         int a = -1;
         bool single = true;
-#pragma unroll
-        for (int t = 0; t < kDecBN; ++t)
-          if (ids_r[t] >= 0) {
-            if (a < 0) a = ids_r[t];
-            else if (ids_r[t] != a) single = false;
+#pragma unroll 16
+        for (int t = 0; t < BN; ++t) {
+          const int id = t < p.T ? __ldg(p.ids + t) : -1;
+          if (id >= 0) {
+            if (a < 0) a = id;
+            else if (id != a) single = false;
           }
+        }
         const int n0 = (u_lo / p.k_blocks) * kDecBM;
         const int jlo = dec_slice_of(p.g, n0), jhi = dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
         if (single && a >= 0 && jlo == jhi) {
@@ -329,7 +334,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (ptx::elect_one()) {
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kDecBM, kDecBN);
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(kDecBM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
         const int kb1 = min(p.k_blocks, kb0 + (u_hi - u));
         ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kDecBN);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
@@ -354,7 +359,8 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
             const uint64_t s_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * L::kA));
 #pragma unroll
             for (int k = 0; k < kDecBK / 16; ++k)
-              ptx::mma_bf16(tmem_base + 32u, s_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              ptx::mma_bf16(tmem_base + (uint32_t)L::kVCol, s_desc + 2 * k, b_desc + 2 * k, idesc,
+                            (kb > kb0 || k > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[stage]);
           if (++stage == p.nstages) {
@@ -382,7 +388,39 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
     // preceding kernel's tail; after the wait only X (L2-resident) is still to be read.
     // lora == 3 (v precomputed, staged): the same groups, with the EXPAND rank re as the rank rows
     const bool lgrp = (LM == 1 && p.lora == 1) || (LM == 2 && p.lora == 3);
-    if (lgrp) {
+    if (BN == 64 && lgrp) {
+      // T <= 64 decode tiles are served only for pools holding ONE adapter (host: capacity == 1), so the batch
+      // has at most one group: the tokens with id >= 0
+      if (we == 0) {
+        const int id0 = (lane < T) ? __ldg(p.ids + lane) : -1;
+        const int id1 = (lane + 32 < T) ? __ldg(p.ids + lane + 32) : -1;
+        s_grp[lane] = id0 >= 0 ? 0 : -1;
+        s_grp[lane + 32] = id1 >= 0 ? 0 : -1;
+        const unsigned m0 = __ballot_sync(0xffffffffu, id0 >= 0), m1 = __ballot_sync(0xffffffffu, id1 >= 0);
+        int a = -1;
+        if (m0) a = __shfl_sync(0xffffffffu, id0, __ffs(m0) - 1);
+        else if (m1) a = __shfl_sync(0xffffffffu, id1, __ffs(m1) - 1);
+        if (lane == 0) {
+          int rows = 0;
+          if (a >= 0) {
+            const SlotEntry e = p.tab[a];
+            rows = min(LM == 2 ? e.re : e.rs, kDecLoraRows);
+            s_gad[0] = a;
+            s_gsc[0] = e.scale;
+            s_grs[0] = rows;
+            s_gq0[0] = 0;
+#pragma unroll
+            for (int j = 0; j < kMaxSlices; ++j) {
+              s_goff[j] = e.offA[j];
+              s_goff[3 + j] = e.offB[j];
+            }
+          }
+          mi[96] = a >= 0 ? 1 : 0;
+          mi[97] = rows;
+        }
+      }
+      ptx::named_bar_sync(1, 128);
+    } else if (lgrp) {
       if (we == 0) {
         // lane t < T holds token t's id; leaders (first token of each id) in token order define the groups
         const int id = (lane < T) ? __ldg(p.ids + lane) : -1;
@@ -485,13 +523,13 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
       const int n = n0 + row;
       const int jlo = dec_slice_of(p.g, n0);
       const int jn = dec_slice_of(p.g, min(n, p.M - 1));
-      float lr[kDecBN];
+      float lr[16];  // LoRA term of the current 16-token chunk (BN == 16: the whole tile)
 #pragma unroll
-      for (int i = 0; i < kDecBN; ++i) lr[i] = 0.f;
+      for (int i = 0; i < 16; ++i) lr[i] = 0.f;
       // tensor-core K-local shrink taken by the producer (same rule): v_seg arrives in TMEM with the accumulator
       const bool tc = CL && LM == 1 && p.tc_shrink && p.lora == 1 && ngroups == 1 && s_grs[0] <= 16 &&
                       jlo == dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
-      if (LM == 1 && p.lora == 1 && ngroups > 0 && !tc) {
+      if constexpr (BN == 16) if (LM == 1 && p.lora == 1 && ngroups > 0 && !tc) {
         // ---- K-local shrink of this segment: v_seg[t][j][k] = s_a sum_{d in seg} X[t][d] A_{a,j}[k][d] -----
         // Thread per 16-byte chunk of the K range, 8 rank rows x 4 tokens per pass: 12 independent loads in
         // flight per chunk (the A rows are L2-resident, X was just written by the preceding kernel), then a
@@ -603,131 +641,136 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
           }
         }
       }
-      if (LM == 2 && p.lora == 3 && ngroups > 0) {
-        // ---- v precomputed (S-LoRA after its collective), B rows staged before the wait: the tile's LoRA
-        // term, added by ONE contributor (whole tile; cluster rank 0; the split tile's first contributor)
-        if (tile != cur_tile) stage_B(tile);
-        const bool mine = whole || (CL ? ptx::cluster_ctarank() == 0
-                                       : cta == dec_cta_of((long long)tile * p.k_blocks, UNITS, GRID));
-        if (mine) {
-          if (T == 1) {
-            const int g = s_grp[0];
-            if (g >= 0) lr[0] = dec_vdot(p, 0, jn, s_B + s_gq0[g] * kDecBM + row, s_grs[g]);
-          } else {
-#pragma unroll
-            for (int t = 0; t < kDecBN; ++t)
-              if (t < T && s_grp[t] >= 0)
-                lr[t] = dec_vdot(p, t, jn, s_B + s_gq0[s_grp[t]] * kDecBM + row, s_grs[s_grp[t]]);
-          }
-        }
-      }
+      // lora == 3 (v precomputed, B staged): the tile's LoRA term is added by ONE contributor (whole tile;
+      // cluster rank 0; the split tile's first contributor)
+      const bool v3 = LM == 2 && p.lora == 3 && ngroups > 0 &&
+                      (whole || (CL ? ptx::cluster_ctarank() == 0
+                                    : cta == dec_cta_of((long long)tile * p.k_blocks, UNITS, GRID)));
+      if (LM == 2 && p.lora == 3 && ngroups > 0 && tile != cur_tile) stage_B(tile);
       if (u == u_lo && etid == 0) DEC_TRACE(3);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       if (u == u_lo && etid == 0) DEC_TRACE(4);
-      uint32_t r[16];
-      ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * kDecBN), r);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
       if (tc) {
-        // v_seg (TMEM lanes k < r/N of the shrink accumulator, read by the lane-quarter-0 warp) -> s_vs, then
-        // lr[t] = s v_seg[t] . B[:, n] for the adapter's tokens (B rows staged before the dependency wait)
+        // v_seg (TMEM lanes k < r/N of the shrink accumulator, read by the lane-quarter-0 warp) -> s_vs
         if (q4 == 0) {
-          uint32_t v16[16];
-          ptx::tmem_ld_32x32b_x16(tmem_base + 32u, v16);
-          ptx::tmem_ld_wait();
           const int rs = s_grs[0];
           const float sc = s_gsc[0];
-          if (lane < rs) {
 #pragma unroll
-            for (int t = 0; t < kDecBN; ++t) s_vs[(t * 3) * kDecLoraRows + lane] = sc * __uint_as_float(v16[t]);
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t v16[16];
+            ptx::tmem_ld_32x32b_x16(tmem_base + (uint32_t)(L::kVCol + c0), v16);
+            ptx::tmem_ld_wait();
+            if (lane < rs) {
+#pragma unroll
+              for (int t = 0; t < 16; ++t) s_vs[(c0 + t) * L::kVsTok + lane] = sc * __uint_as_float(v16[t]);
+            }
           }
         }
         ptx::named_bar_sync(1, 128);
         if (etid == 0) DEC_TRACE(9);
-        // batch 1 (the common decode case) takes a straight-line path: the 16-way guarded unroll below jumps
-        // over 15 cold code blocks (instruction-cache misses on the critical tail)
-        if (T == 1) {
-          if (s_grp[0] == 0) lr[0] = dec_dot(s_vs, s_B + row, s_grs[0]);
-        } else {
-#pragma unroll
-          for (int t = 0; t < kDecBN; ++t)
-            if (t < T && s_grp[t] == 0) lr[t] = dec_dot(s_vs + (t * 3) * kDecLoraRows, s_B + row, s_grs[0]);
-        }
-        if (etid == 0) DEC_TRACE(10);
       }
-      ptx::mbar_arrive(&tempty[acc]);  // the accumulator is in registers: the MMA may reuse it
+      // ---- per 16-token chunk: accumulator -> registers, + LoRA, out (store / DSMEM push / partial) ----------
+      const int sc_cl = CL ? p.cluster : 1;
+      const uint32_t crank = CL ? ptx::cluster_ctarank() : 0u;
+      const int nr_max = (kDecBM + sc_cl - 1) / sc_cl;
+      float* s_slot = reinterpret_cast<float*>(smem + L::kSlotOff);
       if (CL) {
-        // ---- cluster split-K: the s contributors of this tile are this cluster.  Rank c owns rows
-        // [c*128/s, (c+1)*128/s): every contributor pushes its partial rows into the owner's slots (DSMEM,
-        // st.shared::cluster), one cluster barrier, the owner sums in rank order (deterministic), rounds once
-        const int sc = p.cluster;
-        const uint32_t crank = ptx::cluster_ctarank();
-        const int nr_max = (kDecBM + sc - 1) / sc;
-        const int owner = ((row + 1) * sc - 1) / kDecBM;
-        const int rr = row - (owner * kDecBM) / sc;
-        float* s_slot = reinterpret_cast<float*>(smem + L::kSlotOff);
-        const uint32_t dst = ptx::mapa(ptx::smem_u32(s_slot + ((size_t)(crank * nr_max + rr) * kDecBN)), (uint32_t)owner);
-        const int nq = (T + 3) >> 2;
-        ptx::cluster_wait();  // (early arrival) every peer has started
+        ptx::cluster_wait();  // (early arrival) every peer has started: DSMEM pushes below are legal
         if (etid == 0) DEC_TRACE(11);
+      }
+      const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
+      float* my_part = p.part + ((size_t)(cta * 2 + slot) * kDecBM + row) * BN;
+      for (int c0 = 0; c0 < BN && c0 < T; c0 += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN + c0), r);
+        ptx::tmem_ld_wait();
+        const int tn = min(16, T - c0);  // valid tokens of the chunk
+        if (tc) {
+          if (BN == 16 && T == 1) {  // straight-line batch-1 path (no 16-way guarded unroll: i-cache)
+            if (s_grp[0] == 0) lr[0] = dec_dot(s_vs, s_B + row, s_grs[0]);
+          } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q < nq)
-            ptx::st_dsmem_f4(dst + q * 16, __uint_as_float(r[4 * q]) + lr[4 * q], __uint_as_float(r[4 * q + 1]) + lr[4 * q + 1],
-                             __uint_as_float(r[4 * q + 2]) + lr[4 * q + 2], __uint_as_float(r[4 * q + 3]) + lr[4 * q + 3]);
+            for (int i = 0; i < 16; ++i)
+              lr[i] = (i < tn && s_grp[c0 + i] == 0) ? dec_dot(s_vs + (c0 + i) * L::kVsTok, s_B + row, s_grs[0]) : 0.f;
+          }
+        } else if (v3) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int g = (i < tn) ? s_grp[c0 + i] : -1;
+            lr[i] = g >= 0 ? dec_vdot(p, c0 + i, jn, s_B + s_gq0[g] * kDecBM + row, s_grs[g]) : 0.f;
+          }
+        }
+        if (CL) {
+          // cluster split-K: rank c owns rows [c*128/s, (c+1)*128/s); every contributor pushes its partial rows
+          // into the owner's slots (DSMEM)
+          const int owner = ((row + 1) * sc_cl - 1) / kDecBM;
+          const int rr = row - (owner * kDecBM) / sc_cl;
+          const uint32_t dst =
+              ptx::mapa(ptx::smem_u32(s_slot + ((size_t)(crank * nr_max + rr) * BN + c0)), (uint32_t)owner);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (4 * q < tn)
+              ptx::st_dsmem_f4(dst + q * 16, __uint_as_float(r[4 * q]) + lr[4 * q],
+                               __uint_as_float(r[4 * q + 1]) + lr[4 * q + 1], __uint_as_float(r[4 * q + 2]) + lr[4 * q + 2],
+                               __uint_as_float(r[4 * q + 3]) + lr[4 * q + 3]);
+        } else if (whole) {
+          if (LM == 2 && p.lora == 2 && n < p.M) {
+            float lrv[16];
+            dec_vmode_lr(&p, n, c0, tn, lrv);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < tn) lr[i] = lrv[i];
+          }
+          if (n < p.M) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < tn) dec_out<PUSH>(p, par, c0 + i, n, __uint_as_float(r[i]) + lr[i]);
+          }
+        } else {
+          // split tile: this CTA's fp32 partial (its K range, with its K-local LoRA share), [row][BN]
+          float4* my = reinterpret_cast<float4*>(my_part + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (4 * q < tn)
+              __stcg(my + q, make_float4(__uint_as_float(r[4 * q]) + lr[4 * q], __uint_as_float(r[4 * q + 1]) + lr[4 * q + 1],
+                                         __uint_as_float(r[4 * q + 2]) + lr[4 * q + 2],
+                                         __uint_as_float(r[4 * q + 3]) + lr[4 * q + 3]));
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);  // the accumulator was read: the MMA may reuse it
+      if (CL) {
+        // one cluster barrier, then the owner sums its rows over the contributors in rank order (deterministic)
         if (etid == 0) DEC_TRACE(12);
         ptx::cluster_arrive();  // release: my pushes
         ptx::cluster_wait();    // acquire: every peer's rows of my range
         if (etid == 0) DEC_TRACE(6);
-        const int r_lo = (crank * kDecBM) / sc, nr = ((crank + 1) * kDecBM) / sc - r_lo;
+        const int nq = (T + 3) >> 2;
+        const int r_lo = (crank * kDecBM) / sc_cl, nr = ((crank + 1) * kDecBM) / sc_cl - r_lo;
         for (int f = etid; f < nr * nq; f += 128) {
           const int r2 = f % nr, qd = f / nr;
-          float4 y = *reinterpret_cast<const float4*>(s_slot + (size_t)r2 * kDecBN + qd * 4);
-          for (int c = 1; c < sc; ++c) {
-            const float4 z = *reinterpret_cast<const float4*>(s_slot + ((size_t)(c * nr_max + r2) * kDecBN + qd * 4));
+          float4 y = *reinterpret_cast<const float4*>(s_slot + (size_t)r2 * BN + qd * 4);
+          for (int c = 1; c < sc_cl; ++c) {
+            const float4 z = *reinterpret_cast<const float4*>(s_slot + ((size_t)(c * nr_max + r2) * BN + qd * 4));
             y.x += z.x, y.y += z.y, y.z += z.z, y.w += z.w;
           }
           const int nn = n0 + r_lo + r2;
           if (nn < p.M) {
             float yv[4] = {y.x, y.y, y.z, y.w};
             if (LM == 2 && p.lora == 2) {
-              float lrv[kDecBN];
-              dec_vmode_lr(&p, nn, lrv);
+              float lrv[16];
+              dec_vmode_lr(&p, nn, qd * 4, min(4, T - qd * 4), lrv);
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                if (qd * 4 + i < T) yv[i] += lrv[qd * 4 + i];
+                if (qd * 4 + i < T) yv[i] += lrv[i];
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               if (qd * 4 + i < T) dec_out<PUSH>(p, par, qd * 4 + i, nn, yv[i]);
           }
         }
-      } else if (whole) {
-        if (LM == 2 && p.lora == 2 && n < p.M) {
-          float lrv[kDecBN];
-          dec_vmode_lr(&p, n, lrv);
-#pragma unroll
-          for (int t = 0; t < kDecBN; ++t)
-            if (t < T) lr[t] = lrv[t];
-        }
-        if (n < p.M) {
-#pragma unroll
-          for (int t = 0; t < kDecBN; ++t)
-            if (t < T) dec_out<PUSH>(p, par, t, n, __uint_as_float(r[t]) + lr[t]);
-        }
-      } else {
-        // split tile: this CTA's fp32 partial (its K range, with its K-local LoRA share) -> its slot,
-        // [row][16 tokens]: a thread's tokens are one contiguous 64-byte run (float4 stores / loads)
-        const int slot = (tile * p.k_blocks > u_lo) ? 1 : 0;
-        float4* my = reinterpret_cast<float4*>(p.part + ((size_t)(cta * 2 + slot) * kDecBM + row) * kDecBN);
-        const int nq = (T + 3) >> 2;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q < nq)
-            __stcg(my + q, make_float4(__uint_as_float(r[4 * q]) + lr[4 * q], __uint_as_float(r[4 * q + 1]) + lr[4 * q + 1],
-                                       __uint_as_float(r[4 * q + 2]) + lr[4 * q + 2],
-                                       __uint_as_float(r[4 * q + 3]) + lr[4 * q + 3]));
+      } else if (!whole) {
         ptx::named_bar_sync(1, 128);
         const int ts = tile * p.k_blocks;
         const int c_first = dec_cta_of(ts, UNITS, GRID);
@@ -738,43 +781,43 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 ? 1 : 2))
         }
         ptx::named_bar_sync(1, 128);
         if (*s_last) {
-          // finisher: contributors' partials summed in CTA order (deterministic), one rounding
+          // finisher: contributors' partials summed in CTA order (deterministic), 8 contributors' loads in flight
           if (etid == 0) DEC_TRACE(6);
           const int c_last = dec_cta_of(ts + p.k_blocks - 1, UNITS, GRID);
-          // loads of 8 contributors in flight per round, summed in CTA order
-          float y[kDecBN];
+          for (int c0 = 0; c0 < BN && c0 < T; c0 += 16) {
+            const int tn = min(16, T - c0);
+            float y[16];
 #pragma unroll
-          for (int t = 0; t < kDecBN; ++t) y[t] = 0.f;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q < nq) {
+            for (int q = 0; q < 4; ++q) {
               float4 yq = make_float4(0.f, 0.f, 0.f, 0.f);
-              for (int cb = c_first; cb <= c_last; cb += 8) {
-                float4 b8[8];
+              if (4 * q < tn) {
+                for (int cb = c_first; cb <= c_last; cb += 8) {
+                  float4 b8[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const int c = min(cb + e, c_last);
-                  const int sl = (ts > dec_u_lo(c, UNITS, GRID)) ? 1 : 0;
-                  b8[e] = __ldcg(reinterpret_cast<const float4*>(p.part + ((size_t)(c * 2 + sl) * kDecBM + row) * kDecBN) + q);
+                  for (int e = 0; e < 8; ++e) {
+                    const int c = min(cb + e, c_last);
+                    const int sl = (ts > dec_u_lo(c, UNITS, GRID)) ? 1 : 0;
+                    b8[e] = __ldcg(reinterpret_cast<const float4*>(p.part + ((size_t)(c * 2 + sl) * kDecBM + row) * BN + c0) + q);
+                  }
+#pragma unroll
+                  for (int e = 0; e < 8; ++e)
+                    if (cb + e <= c_last) yq.x += b8[e].x, yq.y += b8[e].y, yq.z += b8[e].z, yq.w += b8[e].w;
                 }
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  if (cb + e <= c_last) yq.x += b8[e].x, yq.y += b8[e].y, yq.z += b8[e].z, yq.w += b8[e].w;
               }
               y[4 * q] = yq.x, y[4 * q + 1] = yq.y, y[4 * q + 2] = yq.z, y[4 * q + 3] = yq.w;
             }
-          }
-          if (n < p.M) {
-            if (LM == 2 && p.lora == 2) {
-              float lrv[kDecBN];
-              dec_vmode_lr(&p, n, lrv);
+            if (n < p.M) {
+              if (LM == 2 && p.lora == 2) {
+                float lrv[16];
+                dec_vmode_lr(&p, n, c0, tn, lrv);
 #pragma unroll
-              for (int t = 0; t < kDecBN; ++t)
-                if (t < T) y[t] += lrv[t];
+                for (int i = 0; i < 16; ++i)
+                  if (i < tn) y[i] += lrv[i];
+              }
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (i < tn) dec_out<PUSH>(p, par, c0 + i, n, y[i]);
             }
-#pragma unroll
-            for (int t = 0; t < kDecBN; ++t)
-              if (t < T) dec_out<PUSH>(p, par, t, n, y[t]);
           }
           if (etid == 0) p.cnt[c_first] = 0;  // re-arm for the next launch
         }

@@ -208,7 +208,7 @@ WsLayout ws_layout(const bdlora_pool* p, int64_t T) {
   L.off_umma = o;
   o = align_up(o + bdl::umma_workspace_bytes(p->g.M, (int)T, p->num_sms), 256);
   L.off_dec = o;  // lean decode kernel: split-tile partials
-  if (T <= bdl::kDecMaxT) o = align_up(o + bdl::dec_scratch_bytes(p->num_sms), 256);
+  if (T <= bdl::kDecMaxT) o = align_up(o + bdl::dec_scratch_bytes(p->num_sms, (int)T), 256);
   L.off_route = o;
   const int items = tc_items_max(p, std::min<int64_t>(T, bdl::kRouteMaxSeg));
   if (items > 0) o = align_up(o + sizeof(int) * bdl::RouteLayout::kWords, 256);
@@ -383,6 +383,14 @@ int launch_decode(const bdlora_pool* p, const void* X, int T, const void* W, con
 // chunk) and the batch's distinct adapters to fit the kernel's rank-row capacity in the worst case.
 bool decode_klocal_ok(const bdlora_pool* p, int T) {
   if (p->d.sharding == BDLORA_SHARD_SLORA || p->g.C != 1) return false;
+  if (T > 16) {
+    // 17..64 tokens (BN = 64 tiles): only the tensor-core K-local shrink is compiled there -- one adapter per
+    // pool, r/N <= 16, every tile inside one slice, the arena's A-row map
+    if (p->d.capacity != 1 || p->rs_max > 16 || !p->amap_ok) return false;
+    for (int j = 0; j < p->g.J; ++j)
+      if (p->g.col0[j] % 128) return false;
+    return true;
+  }
   return (int64_t)std::min<int64_t>(T, p->d.capacity) * p->rs_max <= bdl::kDecLoraRowsHost;
 }
 
@@ -394,8 +402,10 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
     // v precomputed: staged-B expand (mode 3) when the batch's distinct adapters fit the kernel's rank-row
     // capacity in the worst case, else the per-output gather (mode 2)
     const bool staged = (int64_t)std::min<int64_t>(T, p->d.capacity) * p->re_max <= bdl::kDecLoraRowsHost;
-    const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, staged ? 3 : 2);
-    if (rc >= 0) return rc;
+    if (T <= 16 || (p->d.capacity == 1 && staged)) {  // 17..64 tokens: one-adapter pools only (BN = 64 tiles)
+      const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, staged ? 3 : 2);
+      if (rc >= 0) return rc;
+    }
   }
   if (bdl::umma_eligible(p->g, T)) {
     const WsLayout L = ws_layout(p, T);
@@ -1169,9 +1179,9 @@ int check_row_push(const bdlora_pool* p, const bdlora_peer* q, int64_t T, const 
     return fail(BDLORA_E_ARG, "%s: peer (nranks=%d, rank=%d) does not match pool (tp_size=%d, tp_rank=%d)", fn,
                 q->nranks, q->rank, p->d.tp_size, p->d.tp_rank);
   if (q->dev != p->dev) return fail(BDLORA_E_ARG, "%s: peer device %d != pool device %d", fn, q->dev, p->dev);
-  if (T > bdl::kDecMaxT || !bdl::dec_eligible(p->g, (int)T) || !decode_klocal_ok(p, (int)T))
+  if (T > bdl::kDecMaxPushT || !bdl::dec_eligible(p->g, (int)T) || !decode_klocal_ok(p, (int)T))
     return fail(BDLORA_E_CAPACITY, "%s: the fused all-reduce serves decode batches (T <= %d, K %% 64 == 0, K-local "
-                "LoRA capacity); T = %lld -- use bdlora_row_forward", fn, bdl::kDecMaxT, (long long)T);
+                "LoRA capacity); T = %lld -- use bdlora_row_forward", fn, bdl::kDecMaxPushT, (long long)T);
   if ((long long)T * p->g.M > q->slot)
     return fail(BDLORA_E_CAPACITY, "%s: T x d_out = %lld exceeds the peer slot (%lld elements)", fn,
                 (long long)T * p->g.M, q->slot);

@@ -180,3 +180,70 @@ def test_decode_v_precomputed_mode(dev, T):
         _assert_tol(_np(Y), _ref(case, i), f"slora v-mode rank {i}")
     for p in pools:
         p.close()
+
+
+# ----------------------------------------------------------------------------- 17..64 tokens (BN = 64 tiles)
+# configs[3] batch 64: one resident adapter per pool -> the decode kernel with 64-token tiles, the tensor-core
+# K-local shrink (BD / NFS) or staged-B expand of a precomputed v (S-LoRA).
+
+@pytest.mark.parametrize("T", [17, 40, 64])
+@pytest.mark.parametrize("pi,n", [(0, 8), (1, 8), (2, 8), (3, 8), (0, 1), (3, 2)])
+def test_decode_bn64_one_adapter(dev, T, pi, n):
+    """70B shapes at TP = N, rank 32 (r/N <= 16 at N >= 2; N = 1 uses the 8B QKV with rank 16), ids 0 with
+    some -1 tokens: every projection, first and last tp_rank, BN = 64 asserted."""
+    rng = synth.rng_for(5800 + T + pi + n, 1)
+    ids = np.where(rng.random(T) < 0.2, -1, 0).astype(np.int32)
+    proj = P70[pi] if n > 1 else P8[pi]
+    r = 32 if n > 1 else 16
+    case = H.make_case(5800 + 10 * pi + n + T, proj, "bd", n, T, ranks=[r], ids=ids)
+    for i in sorted({0, n - 1}):
+        y, info = _run(case, i, dev)
+        assert info["bn"] == 64, info
+        _assert_tol(y, _ref(case, i), f"{proj.name} N={n} T={T} rank {i}")
+
+
+@pytest.mark.parametrize("T", [33, 64])
+def test_decode_bn64_integer_bit_exact(dev, T):
+    """P10 at 64-token tiles: column (3 slices, 128-aligned) and row, N = 4, bit-identical to the oracle."""
+    for proj in (synth.Projection("qkv", "column", 2048, (1024, 512, 512)), synth.Projection("down", "row", 4096, (1024,))):
+        case = H.make_case(5900 + T, proj, "bd", 4, T, ranks=[32], integer=True, ids=np.zeros(T, np.int32))
+        for i in (0, 3):
+            y, info = _run(case, i, dev)
+            assert info["bn"] == 64, info
+            ref = ol.bf16_round(_ref(case, i))
+            assert np.array_equal(y, ref), f"{proj.name} T={T} rank {i}: {np.count_nonzero(y != ref)} mismatches"
+
+
+@pytest.mark.parametrize("T", [24, 64])
+def test_decode_bn64_nfs_and_slora(dev, T):
+    """NFS-LoRA (K-local) and S-LoRA (v precomputed, staged B) at 64-token tiles, one adapter per pool."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    ids = np.zeros(T, np.int32)
+    case = H.make_case(5950 + T, P70[1], "nfs", 8, T, ranks=[16], ids=ids)
+    y, info = _run(case, 7, dev)
+    assert info["bn"] == 64
+    _assert_tol(y, _ref(case, 7), "nfs row")
+    proj = P70[0]
+    n = 2
+    case = H.make_case(5960 + T, proj, "slora", n, T, ranks=[16], ids=ids)
+    pools = [H.make_pool(case, i) for i in range(n)]
+    vs = []
+    for i, p in enumerate(pools):
+        X, W, idt = H.device_inputs(case, i, dev)
+        v = torch.zeros(bd.bdlora_v_elems(p, T), dtype=torch.float32, device=dev)
+        bd.bdlora_lora_shrink(p, X, idt, v, bd.make_workspace(p, T))
+        vs.append(v)
+    vg = torch.cat(vs)
+    for i, p in enumerate(pools):
+        X, W, idt = H.device_inputs(case, i, dev)
+        Y = torch.empty(T, p.m_loc, dtype=torch.bfloat16, device=dev)
+        bd.bdlora_base_expand(p, X, W, idt, vg, Y, bd.make_workspace(p, T))
+        info = bd.bdlora_last_launch_info()
+        assert info["kind"] == 3 and info["bn"] == 64, info
+        torch.cuda.synchronize()
+        _assert_tol(_np(Y), _ref(case, i), f"slora v-mode T={T} rank {i}")
+    for p in pools:
+        p.close()
