@@ -244,7 +244,9 @@ int bdlora_last_launch_info(int32_t info[8]);
 /* ---------------------------------------------------------------- routing metadata (a2) ----- */
 /* Segments = maximal runs of equal consecutive ids in token order (reading R10): writes
    seg_start/seg_len/seg_id[0..n) and *n_seg_dev = n (all device int32 arrays of >= T entries).
-   Bit-exact with the oracle's RLE.  Used by the prefill (SGMV) path; exposed for testing.       */
+   Bit-exact with the oracle's RLE.  The forwards do not consume it: they group tokens by adapter
+   (route_kernel for T > 64, the decode kernels' group tables for T <= 64), which merges runs of the
+   same id; this entry point exposes the SGMV segment view for callers (e.g. a scheduler) and tests. */
 int bdlora_build_segments(const int32_t* ids, int64_t T, int32_t* seg_start, int32_t* seg_len,
                           int32_t* seg_id, int32_t* n_seg_dev, bdlora_stream_t stream);
 

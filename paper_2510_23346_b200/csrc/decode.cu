@@ -52,7 +52,7 @@ int env_int(const char* name, int dflt) {
 template <int S, bool CL, int LM, bool PUSH, int BN>
 int launch_one(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
                cudaStream_t st) {
-  using L = DecSmem<S, CL, BN>;
+  using L = DecSmem<S, CL, BN, LM>;
   static bool attr[kMaxDev] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -104,9 +104,17 @@ int launch_bn64(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& t
   return launch_one<6, CL, 1, false, 64>(p, tmW, tmX, tmA, st);
 }
 
+// multi-adapter expand of a precomputed v (lora 4): BN = 64 tiles, 4-stage ring (the group tables, two B-row
+// chunk buffers and the tile's LoRA terms take the rest of the shared memory)
+template <bool CL>
+int launch_mt(const DecParams& p, const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmA,
+              cudaStream_t st) {
+  return launch_one<kDecMtStages, CL, 3, false, 64>(p, tmW, tmX, tmA, st);
+}
+
 // Largest cluster size c in [2, want] such that `need` clusters of instantiation <S, true> are co-resident
 // (one wave: every tile's contributors run at once), cached per (device, S, size); 1 if none.
-template <int S, int BN = 16>
+template <int S, int BN = 16, int LM = 1>
 int fit_cluster(int want, int need) {
   static int cache[kMaxDev][kDecMaxCluster + 1];
   static bool init = false;
@@ -121,13 +129,13 @@ int fit_cluster(int want, int need) {
   for (int c = want; c >= 2; --c) {
     int& mc = cache[dev][c];
     if (mc < 0) {
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, LM, false, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            227 * 1024);
-      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, 1, false, BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(dec_lora_gemm_kernel<S, true, LM, false, BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t qc = {};
       qc.gridDim = dim3(c * need);
       qc.blockDim = dim3(kDecThreads);
-      qc.dynamicSmemBytes = DecSmem<S, true, BN>::kBytes;
+      qc.dynamicSmemBytes = DecSmem<S, true, BN, LM>::kBytes;
       cudaLaunchAttribute ca[1];
       ca[0].id = cudaLaunchAttributeClusterDimension;
       ca[0].val.clusterDim.x = c;
@@ -135,7 +143,7 @@ int fit_cluster(int want, int need) {
       ca[0].val.clusterDim.z = 1;
       qc.attrs = ca;
       qc.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<S, true, 1, false, BN>, &qc) != cudaSuccess) {
+      if (cudaOccupancyMaxActiveClusters(&mc, (void*)dec_lora_gemm_kernel<S, true, LM, false, BN>, &qc) != cudaSuccess) {
         cudaGetLastError();
         mc = 0;
       }
@@ -147,9 +155,24 @@ int fit_cluster(int want, int need) {
 
 }  // namespace
 
+int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* ids, const SlotEntry* tab,
+                      const __nv_bfloat16* arena, float* v, int num_sms, cudaStream_t st, int pdl) {
+  if (T < 1 || T > kDecMaxT) return 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::max(1, 2 * num_sms));  // two items per CTA, grid-stride; leaves room for the GEMM's CTAs
+  cfg.blockDim = dim3(kDecShrinkThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, dec_shrink_kernel, X, T, ids, tab, arena, g, v, pdl) == cudaSuccess ? 0 : -1;
+}
+
 size_t dec_counter_bytes() { return sizeof(int) * kDecMaxGrid; }
 size_t dec_scratch_bytes(int num_sms, int T) {
-  const int bn = T <= 16 ? 16 : 64;
+  const int bn = 64;  // multi-adapter batches (lora 4) take BN = 64 tiles at any T
   return (size_t)std::min(num_sms, kDecMaxGrid) * 2 * bn * kDecBM * 4;
 }
 bool dec_eligible(const Geom& g, int T) { return T >= 1 && T <= kDecMaxT && g.K % kDecBK == 0 && g.K >= kDecBK; }
@@ -181,9 +204,16 @@ int dec_launch(const DecLaunch& a) {
   // projections.  tiles > #SM: stream-K over a grid that divides the tile count when such a grid keeps
   // >= 70% of the SMs busy (whole tiles per CTA, no split tiles), else over every SM.
   const int tiles = p.m_tiles;
-  const bool bn64 = a.T > 16;  // 17..64 tokens: BN = 64 token tile (the caller guarantees one adapter per pool)
+  // 17..64 tokens (the caller guarantees one adapter per pool for lora 1 / 3) and every multi-adapter expand
+  // (lora 4): BN = 64 token tiles
+  const bool mt = a.lora == 4;
+  const bool bn64 = a.T > 16 || mt;
   const int BNh = bn64 ? 64 : 16;
   if (bn64 && a.push) return 1;
+  // BN = 64 tiles compile only the tensor-core K-local shrink (lora 1): without the arena's A-row map (or with
+  // the tensor-core shrink switched off) the caller's multi-kernel path serves the batch
+  const bool tc_ok = a.amap != nullptr && env_int("BDLORA_DEC_TC_SHRINK", 1) != 0;
+  if (bn64 && a.lora == 1 && !tc_ok) return 1;
   long long grid;
   const int min_kb = std::max(1, env_int("BDLORA_DEC_MINKB", 1));
   p.cluster = 1;
@@ -199,7 +229,9 @@ int dec_launch(const DecLaunch& a) {
     if (s >= 2 && cl_max >= 2) {
       const int want = std::min(s, cl_max);
       int c = 1;
-      if (bn64) {
+      if (mt) {
+        c = fit_cluster<kDecMtStages, 64, 3>(want, tiles);
+      } else if (bn64) {
         c = fit_cluster<6, 64>(want, tiles);
       } else {
         if (deep_kb > 0 && p.k_blocks / want >= deep_kb) {
@@ -251,7 +283,7 @@ int dec_launch(const DecLaunch& a) {
   // per SM: the PDL overlap with the next projection matters little next to a 30+ us stream); the rest keep
   // <= 113 KB so two CTAs share an SM across projection boundaries.
   if (tiles > sms) deep = deep_kb > 0 && units / p.grid >= deep_kb;
-  const int smax = bn64 ? 6 : deep ? 8 : p.cluster > 1 ? 4 : 5;
+  const int smax = mt ? kDecMtStages : bn64 ? 6 : deep ? 8 : p.cluster > 1 ? 4 : 5;
   const int stages = std::min(smax, std::max(2, env_int("BDLORA_DEC_STAGES", smax)));
   p.nstages = stages;
   if (a.grid_out) *a.grid_out = p.grid;
@@ -264,8 +296,9 @@ int dec_launch(const DecLaunch& a) {
   g_dec_last[6] = 1;
   g_dec_last[7] = p.k_blocks;
   // the arena's A-row map when the pool has one (else a dummy: the tensor-core shrink is then off)
-  p.tc_shrink = (a.amap != nullptr && env_int("BDLORA_DEC_TC_SHRINK", 1) != 0) ? 1 : 0;
+  p.tc_shrink = tc_ok ? 1 : 0;
   const CUtensorMap& tmA = a.amap ? *a.amap : tmX;
+  if (mt) return p.cluster > 1 ? launch_mt<true>(p, tmW, tmX, tmA, a.stream) : launch_mt<false>(p, tmW, tmX, tmA, a.stream);
   if (bn64) return p.cluster > 1 ? launch_bn64<true>(p, tmW, tmX, tmA, a.stream) : launch_bn64<false>(p, tmW, tmX, tmA, a.stream);
   if (p.cluster > 1)
     return deep ? launch_stages<8, true>(p, tmW, tmX, tmA, a.stream) : launch_stages<4, true>(p, tmW, tmX, tmA, a.stream);

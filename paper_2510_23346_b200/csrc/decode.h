@@ -25,7 +25,8 @@ struct DecLaunch {
   int num_sms;
   cudaStream_t stream;
   int pdl;
-  int lora;                   // 1 K-local, 2 v precomputed (per-output gather), 3 v precomputed (B rows staged)
+  int lora;                   // 1 K-local, 2 v precomputed (per-output gather), 3 v precomputed (B rows staged),
+                              // 4 v precomputed, any number of adapters (B rows streamed in chunks, BN = 64)
   const CUtensorMap* amap;    // the pool arena as [rows, K] bf16 with 16-row boxes (tensor-core K-local shrink), or null
   int push;                   // 1: fused row all-reduce -- fp32 partial pushed to every rank of `peer` (not Y)
   PeerDev peer;
@@ -42,6 +43,10 @@ bool dec_eligible(const Geom& g, int T);
 bool dec_enabled();                        // BDLORA_DECODE=0 selects the older single-kernel forward
 // Returns 0 on launch, non-zero if the shape is not handled (caller falls back), negative on a CUDA error.
 int dec_launch(const DecLaunch& a);
+// Multi-adapter shrink of a T <= 64 batch into v [T][J][Rc] fp32 (dec_shrink_kernel).  0 on launch, 1 if T is
+// out of range, negative on a CUDA error.
+int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* ids, const SlotEntry* tab,
+                      const __nv_bfloat16* arena, float* v, int num_sms, cudaStream_t st, int pdl);
 void dec_last_launch(int info[8]);
 void dec_set_trace(long long* buf);
 

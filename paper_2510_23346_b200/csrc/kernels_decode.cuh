@@ -38,6 +38,7 @@ constexpr int kDecLoraRows = 32;   // K-local: sum over the batch's distinct ada
 constexpr int kDecMaxGroups = 16;  // distinct adapters of a <= 16-token batch
 constexpr int kDecMaxGrid = 1024;  // split-tile counters (indexed by the first contributor CTA)
 constexpr int kDecMaxCluster = 16; // cluster split-K: contributors of one tile (non-portable size above 8)
+constexpr int kDecMtStages = 4;    // ring depth of the multi-adapter (LM 3) instantiation
 
 struct DecParams {
   int M, K, T;
@@ -73,14 +74,36 @@ __device__ __forceinline__ void dec_out(const DecParams& p, int par, int t, int 
   }
 }
 
-template <int S, bool CL, int BN = 16>
+// LM 3 (multi-adapter expand of a precomputed v): adapter-group tables of up to 64 tokens / 64 groups
+struct alignas(16) DecGroups {
+  int ids[64];      // token ids (-1 past T)
+  int grp[64];      // group of each token (-1 = no adapter)
+  int lgid[64];     // group index of each leader token
+  int gad[64];      // adapter id of each group (order of first appearance)
+  int grs[64];      // shrink rank rows (A rows on this device)
+  int gre[64];      // expand rank rows (B rows on this device)
+  int gq0[64];      // first expand row of the group in the batch's row numbering (prefix of gre)
+  int gp0[64];      // prefix of grs (the shrink's item numbering)
+  int gcnt[64];     // member tokens
+  int gst[64];      // first member in gmem
+  int gmem[64];     // member tokens, grouped, token order inside a group
+  float gsc[64];    // s_a
+  long long goffA[64][kMaxSlices];
+  long long goffB[64][kMaxSlices];
+  unsigned lm[2];
+  int ngroups, qtot, ptot, pad;
+};
+
+template <int S, bool CL, int BN = 16, int LM = 1>
 struct DecSmem {
+  static constexpr bool kMt = LM == 3;           // multi-adapter expand of a precomputed v (BN = 64 only)
   static constexpr int kW = kDecBM * kDecBK * 2;  // 16 KB weight tile
   static constexpr int kX = BN * kDecBK * 2;      // token tile (2 KB at BN = 16)
   // CL: a 16-row box of the batch's adapter A rows per stage (tensor-core K-local shrink).  The ring sits
   // FIRST: the shrink MMA's operand is 128 rows (M = 128), rows 16..127 -- ignored TMEM lanes -- read the
   // next 14 KB of this CTA's own shared memory (following boxes and the weight ring), never past it
-  static constexpr int kA = CL ? 16 * kDecBK * 2 : 0;
+  static constexpr int kTcShrink = !kMt && (CL || BN == 64);   // instantiations with the tensor-core K-local shrink
+  static constexpr int kA = kTcShrink ? 16 * kDecBK * 2 : 0;
   static constexpr int kWOff = S * kA;
   static constexpr int kXOff = kWOff + S * kW;
   static constexpr int kBarOff = kXOff + S * kX;
@@ -88,21 +111,30 @@ struct DecSmem {
   // misc ints: [0,16) ids  [16,32) group of token  [32,48) group adapter  [48,64) group rs  [64,80) group row
   // offset q0  [80,96) member masks  [96] n_groups  [97] rows total ; floats [128,144) group scale ;
   // long long [160 + 2*(g*3 + j)) group A / B offsets per slice (as int pairs)
-  // ... [960, 1024) group of each of up to 64 tokens
-  static constexpr int kMiscBytes = 4096;
+  // ... [960, 1024) group of each of up to 64 tokens.  LM 3: a DecGroups.
+  static constexpr int kMiscBytes = kMt ? 8192 : 4096;
+  static_assert(!kMt || sizeof(DecGroups) <= kMiscBytes, "group tables");
   // v_seg: BN = 16: [16 tokens][3 slices][32] fp32; BN = 64 (one adapter, one slice per tile): [64][32]
   static constexpr int kVsTok = BN == 16 ? 3 * kDecLoraRows : kDecLoraRows;
   static constexpr int kVsOff = kMiscOff + kMiscBytes;
-  static constexpr int kVsBytes = BN * kVsTok * 4;
-  static constexpr int kBOff = kVsOff + kVsBytes;               // B rows [32][128] bf16 of the tile's columns
-  static constexpr int kBBytes = kDecLoraRows * kDecBM * 2;
+  static constexpr int kVsBytes = kMt ? 0 : BN * kVsTok * 4;
+  // B rows of the tile's columns: [32][128] bf16; LM 3: two 64-row chunk buffers (cp.async double buffering)
+  static constexpr int kBOff = kVsOff + kVsBytes;
+  static constexpr int kMtRows = 64;
+  static constexpr int kBBytes = kMt ? 2 * kMtRows * kDecBM * 2 : kDecLoraRows * kDecBM * 2;
+  // LM 3: the tile's LoRA terms [64 tokens][128 columns] fp32 (a thread owns one column)
+  static constexpr int kLrOff = kBOff + kBBytes;
+  static constexpr int kLrBytes = kMt ? 64 * kDecBM * 4 : 0;
+  // LM 3: v of the tile's slice staged once, [T][C * Rc] fp32 (when it fits)
+  static constexpr int kVmOff = kLrOff + kLrBytes;
+  static constexpr int kVmFloats = kMt ? 4096 : 0;
   // cluster split-K: [s][ceil(128/s)][16] fp32 partial slots the peers push into (<= (128 + s) x 16 floats)
-  static constexpr int kSlotOff = kBOff + kBBytes;
+  static constexpr int kSlotOff = kVmOff + kVmFloats * 4;
   static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * BN * 4 : 0;
   static constexpr int kBytes = kSlotOff + kSlotBytes + 1024;   // + 1024-B alignment slack
-  static constexpr int kVCol = 2 * BN;                          // TMEM: [acc 0 | acc 1 | v_seg (CL)]
-  static constexpr int kTmemCols = BN == 16 ? (CL ? 64 : 32) : 256;
-  static_assert(S > 5 || kBytes <= 113 * 1024, "two CTAs per SM");
+  static constexpr int kVCol = 2 * BN;                          // TMEM: [acc 0 | acc 1 | v_seg 0 | v_seg 1]
+  static constexpr int kTmemCols = BN == 16 ? (CL ? 64 : 32) : (kMt ? 128 : 256);
+  static_assert(S > 5 || BN > 16 || kBytes <= 113 * 1024, "two CTAs per SM");
   static_assert(kBytes <= 227 * 1024, "shared memory per CTA");
 };
 
@@ -114,6 +146,196 @@ struct DecSmem {
       p.trace[(size_t)blockIdx.x * 32 + (slot)] = t_;                 \
     }                                                                 \
   } while (0)
+
+// Adapter groups of a batch of T <= 64 tokens (distinct ids in order of first appearance), built
+// by every thread of a barrier group of >= 64 threads (tid 0..; whole warps), `sync` = that group's barrier.
+// ids and the slot table are never written by the kernel preceding a forward (bdlora_set_pdl contract), so
+// this runs before the programmatic-dependency wait.
+template <class Sync>
+__device__ __forceinline__ void dec_groups64(DecGroups& G, const int* __restrict__ ids, int T,
+                                             const SlotEntry* __restrict__ tab, int tid, Sync sync) {
+  if (tid < 64) G.ids[tid] = tid < T ? __ldg(ids + tid) : -1;
+  sync();
+  int id = -1, first = 64, pos = 0, cnt_all = 0;
+  if (tid < 64) {
+    // all 64 ids through 16 broadcast 16-byte loads, compared in registers (no dependent shared-memory chain)
+    id = G.ids[tid];
+    const int4* v4 = reinterpret_cast<const int4*>(G.ids);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int4 w = v4[q];
+      const int o[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int t2 = 4 * q + e;
+        const bool eq = o[e] == id;
+        first = (eq && t2 < first) ? t2 : first;
+        pos += (eq && t2 < tid) ? 1 : 0;
+        cnt_all += eq ? 1 : 0;
+      }
+    }
+  }
+  const bool lead = id >= 0 && first == tid;
+  const unsigned bm = __ballot_sync(0xffffffffu, lead);
+  if (tid < 64 && (tid & 31) == 0) G.lm[tid >> 5] = bm;
+  sync();
+  const unsigned lm0 = G.lm[0], lm1 = G.lm[1];
+  if (lead) {
+    const int lane = tid & 31;
+    const int gi = tid < 32 ? __popc(lm0 & ((1u << lane) - 1u)) : __popc(lm0) + __popc(lm1 & ((1u << lane) - 1u));
+    G.lgid[tid] = gi;
+    const SlotEntry e = tab[id];
+    G.gad[gi] = id;
+    G.gsc[gi] = e.scale;
+    G.grs[gi] = e.rs;
+    G.gre[gi] = e.re;
+#pragma unroll
+    for (int j = 0; j < kMaxSlices; ++j) {
+      G.goffA[gi][j] = e.offA[j];
+      G.goffB[gi][j] = e.offB[j];
+    }
+    G.gcnt[gi] = cnt_all;
+  }
+  sync();
+  if (tid < 64) G.grp[tid] = id >= 0 ? G.lgid[first] : -1;  // first <= tid is a leader when id >= 0
+  if (tid < 32) {  // exclusive prefixes over the groups (two per lane): expand rows, shrink rows, members
+    const int ng = __popc(lm0) + __popc(lm1);
+    const int g0 = 2 * tid, g1 = 2 * tid + 1;
+    const int e0 = g0 < ng ? G.gre[g0] : 0, e1 = g1 < ng ? G.gre[g1] : 0;
+    const int s0 = g0 < ng ? G.grs[g0] : 0, s1 = g1 < ng ? G.grs[g1] : 0;
+    const int c0 = g0 < ng ? G.gcnt[g0] : 0, c1 = g1 < ng ? G.gcnt[g1] : 0;
+    int ie = e0 + e1, is = s0 + s1, ic = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ye = __shfl_up_sync(0xffffffffu, ie, o), ys = __shfl_up_sync(0xffffffffu, is, o),
+                yc = __shfl_up_sync(0xffffffffu, ic, o);
+      if (tid >= o) ie += ye, is += ys, ic += yc;
+    }
+    const int xe = ie - e0 - e1, xs = is - s0 - s1, xc = ic - c0 - c1;
+    if (g0 < ng) G.gq0[g0] = xe, G.gp0[g0] = xs, G.gst[g0] = xc;
+    if (g1 < ng) G.gq0[g1] = xe + e0, G.gp0[g1] = xs + s0, G.gst[g1] = xc + c0;
+    if (tid == 31) G.ngroups = ng, G.qtot = ie, G.ptot = is;
+  }
+  sync();
+  if (tid < 64 && id >= 0) G.gmem[G.gst[G.grp[tid]] + pos] = tid;
+  sync();
+}
+
+// group holding row q of a prefix table (largest g < ng with pre[g] <= q)
+__device__ __forceinline__ int dec_find_group(const int* pre, int ng, int q) {
+  int lo = 0, hi = ng - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= q) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Multi-adapter LoRA shrink of a decode batch (matmul_3 / matmul_5 for T <= 64 tokens over many adapters,
+// P:287-288):  v[t][j][k] = s_a(t) X[t] . A_{a(t),j}[k]  (fp32, scaled; layout [T][J][Rc]).
+// Work item = one A row (group g, slice j, rank row k): read from HBM exactly once, dotted with every member
+// token of the group.  Four warps share an item (one K quarter each, 16-byte loads, 8 in flight per lane),
+// fixed-order reduction (deterministic).  Launched before the decode GEMM with programmatic dependent launch:
+// the GEMM streams its weights while this runs.
+constexpr int kDecShrinkThreads = 256;
+__global__ void __launch_bounds__(kDecShrinkThreads) dec_shrink_kernel(const __nv_bfloat16* __restrict__ X, int T,
+                                                                       const int* __restrict__ ids,
+                                                                       const SlotEntry* __restrict__ tab,
+                                                                       const __nv_bfloat16* __restrict__ arena, Geom g,
+                                                                       float* __restrict__ v, int pdl) {
+  __shared__ DecGroups G;
+  __shared__ float s_red[2][4][4];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  dec_groups64(G, ids, T, tab, tid, [] { __syncthreads(); });
+  if (tid == 0) ptx::pdl_launch_dependents();  // the GEMM may start streaming its weights
+  if (pdl) ptx::pdl_wait();                    // X is written by the preceding kernel
+  const int J = g.J, K = g.K, ng = G.ngroups;
+  const int items = J * G.ptot;
+  const int half = warp >> 2, quarter = warp & 3;  // two items per CTA, four warps per item
+  const int nch = K >> 3;                          // 16-byte chunks of a row
+  const int c_lo = (nch * quarter) >> 2, c_hi = (nch * (quarter + 1)) >> 2;
+  for (int it0 = blockIdx.x * 2; it0 < items; it0 += gridDim.x * 2) {
+    const int it = it0 + half;
+    const bool valid = it < items;
+    int gi = 0, j = 0, k = 0;
+    if (valid) {
+      // item -> (group, slice, row): groups own J * rs consecutive items, slice-major inside a group
+      int lo = 0, hi = ng - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (J * G.gp0[mid] <= it) lo = mid;
+        else hi = mid - 1;
+      }
+      gi = lo;
+      const int r = it - J * G.gp0[gi];
+      j = r / G.grs[gi];
+      k = r - j * G.grs[gi];
+    }
+    const int cnt = valid ? G.gcnt[gi] : 0;
+    const __nv_bfloat16* Arow = arena + G.goffA[gi][j] + (size_t)k * K;
+    for (int tb = 0; tb < 64; tb += 4) {  // member tokens, 4 per pass (block-uniform trip count)
+      const int ntb = __syncthreads_or(tb < cnt);
+      if (!ntb) break;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      int tok[4];
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) tok[qq] = (tb + qq < cnt) ? G.gmem[G.gst[gi] + tb + qq] : -1;
+      if (tb < cnt) {
+        // blocks of 8 chunks per lane (256 per warp): the 8 A loads, then 2 tokens' 16 X loads, all in flight
+#pragma unroll 1
+        for (int cb = c_lo; cb < c_hi; cb += 256) {
+          uint4 av[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int cc = cb + lane + 32 * u;
+            av[u] = cc < c_hi ? ld_cached_u4(Arow + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int qp = 0; qp < 4; qp += 2) {
+            if (tb + qp < cnt) {
+              const __nv_bfloat16* xr0 = X + (size_t)tok[qp] * K;
+              const __nv_bfloat16* xr1 = X + (size_t)(tok[qp + 1] >= 0 ? tok[qp + 1] : tok[qp]) * K;
+              uint4 x0[8], x1[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int cc = cb + lane + 32 * u;
+                x0[u] = cc < c_hi ? ld_cached_u4(xr0 + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
+                x1[u] = cc < c_hi ? ld_cached_u4(xr1 + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                float af[8], f0[8], f1[8];
+                bf16x8_to_f32(av[u], af);
+                bf16x8_to_f32(x0[u], f0);
+                bf16x8_to_f32(x1[u], f1);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  acc[qp] = fmaf(af[e], f0[e], acc[qp]);
+                  acc[qp + 1] = fmaf(af[e], f1[e], acc[qp + 1]);
+                }
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) acc[qq] = warp_sum(acc[qq]);
+      if (lane == 0) {
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) s_red[half][quarter][qq] = acc[qq];
+      }
+      __syncthreads();
+      const int tq = lane == 0 ? tok[0] : lane == 1 ? tok[1] : lane == 2 ? tok[2] : tok[3];
+      if (quarter == 0 && lane < 4 && tq >= 0) {
+        const int qq = lane;
+        const float sum = (s_red[half][0][qq] + s_red[half][1][qq]) + (s_red[half][2][qq] + s_red[half][3][qq]);
+        v[((size_t)tq * J + j) * g.Rc + k] = G.gsc[gi] * sum;
+      }
+      __syncthreads();
+    }
+  }
+}
 
 __device__ __forceinline__ int dec_u_lo(long long c, int units, int grid) { return (int)(c * units / grid); }
 __device__ __forceinline__ int dec_cta_of(long long u, int units, int grid) {
@@ -174,6 +396,21 @@ __device__ __forceinline__ float dec_dot(const float* vs, const uint16_t* sb, in
   return s0;
 }
 
+// v_seg[t][0..15] . b[0..15] (rows past r/N are zero on both sides), two interleaved accumulators
+__device__ __forceinline__ float dec_dot16(const float* vs, const float (&bq)[16]) {
+  const float4* v4 = reinterpret_cast<const float4*>(vs);
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 a = v4[q];
+    s0 = fmaf(a.x, bq[4 * q], s0);
+    s1 = fmaf(a.y, bq[4 * q + 1], s1);
+    s0 = fmaf(a.z, bq[4 * q + 2], s0);
+    s1 = fmaf(a.w, bq[4 * q + 3], s1);
+  }
+  return s0 + s1;
+}
+
 // lora == 3: s v[t][j] . B[:, n] over the expand rank re, v [C][T][J][Rc] fp32 (rank row k = c * re/C + kk)
 __device__ __forceinline__ float dec_vdot(const DecParams& p, int t, int j, const uint16_t* sb, int re) {
   const int C = p.g.C, rc = re / C;
@@ -191,8 +428,9 @@ template <int S, bool CL, int LM, bool PUSH, int BN = 16>
 __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
     dec_lora_gemm_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                          const __grid_constant__ CUtensorMap tmA, const __grid_constant__ DecParams p) {
-  using L = DecSmem<S, CL, BN>;
+  using L = DecSmem<S, CL, BN, LM>;
   static_assert(BN == 16 || BN == 64, "token tile");
+  static_assert(LM != 3 || (BN == 64 && !PUSH), "multi-adapter expand: BN = 64 tiles");
   static_assert(!PUSH || LM == 1, "the fused all-reduce serves the K-local (BD / NFS) path");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -217,7 +455,8 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
   float* s_vs = (float*)(smem + L::kVsOff);
   float* s_red = (float*)(mi + 512);             // [4 warps][32] cross-warp partial dots
   int* s_gtok = mi + 640;                         // [group][16] member tokens in token order
-  int* s_tcflag = mi + 900;                       // producer's tensor-core-shrink decision (read by the MMA warp)
+  // producer's tensor-core-shrink decision (read by the MMA warp); LM 3: past the group tables
+  int* s_tcflag = L::kMt ? mi + (L::kMiscBytes / 4 - 4) : mi + 900;
   uint16_t* s_B = (uint16_t*)(smem + L::kBOff);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -280,8 +519,14 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
       // stage and the MMA warp accumulates v_seg = A_seg X_seg^T in TMEM.  Same rule as the epilogue's.
       // ids and the slot table are read before the dependency (bdlora_set_pdl contract).
       bool use_tc = false;
-      int arow = 0;
-      if (CL && LM == 1 && p.lora == 1 && p.tc_shrink && nu > 0) {
+      int arow_j[kMaxSlices] = {0, 0, 0};  // the adapter's first A row of each slice (arena row coordinate)
+      // a CTA of a stream-K grid may own tiles of different slices (every tile inside one slice): the box row
+      // follows the tile of each stage
+      auto arow_of = [&](int u) {
+        const int j = dec_slice_of(p.g, (u / p.k_blocks) * kDecBM);
+        return j == 0 ? arow_j[0] : j == 1 ? arow_j[1] : arow_j[2];
+      };
+      if (L::kTcShrink && LM == 1 && p.lora == 1 && p.tc_shrink && nu > 0) {
         int a = -1;
         bool single = true;
 #pragma unroll 16
@@ -298,14 +543,15 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
           const SlotEntry e = p.tab[a];
           if (e.rs <= 16) {
             use_tc = true;
-            arow = (int)(e.offA[jlo] / p.K);
+#pragma unroll
+            for (int j = 0; j < kMaxSlices; ++j) arow_j[j] = j < p.g.J ? (int)(e.offA[j] / p.K) : 0;
           }
         }
         if (use_tc)
           for (int idx = 0; idx < P; ++idx) {
             const int u = u_lo + idx, kb = u - (u / p.k_blocks) * p.k_blocks;
             ptx::mbar_expect_tx(&full[idx], L::kA);
-            ptx::tma_load_2d(sA + idx * L::kA, &tmA, &full[idx], kb * kDecBK, arow, pol_x);
+            ptx::tma_load_2d(sA + idx * L::kA, &tmA, &full[idx], kb * kDecBK, arow_of(u), pol_x);
           }
       }
       *s_tcflag = use_tc ? 1 : 0;  // published to the MMA warp by the arrivals on full[] below
@@ -324,7 +570,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         ptx::mbar_arrive_expect_tx(&full[stage], L::kW + L::kX + (use_tc ? L::kA : 0));
         ptx::tma_load_2d(sW + stage * L::kW, &tmW, &full[stage], kb * kDecBK, tile * kDecBM, pol_w);
         ptx::tma_load_2d(sX + stage * L::kX, &tmX, &full[stage], kb * kDecBK, 0, pol_x);
-        if (use_tc) ptx::tma_load_2d(sA + stage * L::kA, &tmA, &full[stage], kb * kDecBK, arow, pol_x);
+        if (use_tc) ptx::tma_load_2d(sA + stage * L::kA, &tmA, &full[stage], kb * kDecBK, arow_of(u), pol_x);
         if (++stage == NS) {
           stage = 0;
           phase ^= 1;
@@ -355,11 +601,11 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
 #pragma unroll
           for (int k = 0; k < kDecBK / 16; ++k)
             ptx::mma_bf16(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-          if (CL && *s_tcflag) {  // K-local shrink: V[k][t] += A_a[k][kb] . X[t][kb]  (lanes >= r/N ignored)
+          if (L::kTcShrink && *s_tcflag) {  // K-local shrink: V[k][t] += A_a[k][kb] . X[t][kb]  (lanes >= r/N ignored)
             const uint64_t s_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * L::kA));
 #pragma unroll
             for (int k = 0; k < kDecBK / 16; ++k)
-              ptx::mma_bf16(tmem_base + (uint32_t)L::kVCol, s_desc + 2 * k, b_desc + 2 * k, idesc,
+              ptx::mma_bf16(tmem_base + (uint32_t)(L::kVCol + acc * BN), s_desc + 2 * k, b_desc + 2 * k, idesc,
                             (kb > kb0 || k > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[stage]);
@@ -508,6 +754,63 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
                               (uint32_t)(d_hi - d_lo) * 2);
       }
     }
+    // ---- LM 3: adapter groups of the batch; the first segment's first chunk of B rows staged before the wait
+    DecGroups& G = *reinterpret_cast<DecGroups*>(mi);
+    uint16_t* s_Bm = reinterpret_cast<uint16_t*>(smem + L::kBOff);
+    float* s_lr = reinterpret_cast<float*>(smem + L::kLrOff);
+    // this contributor's share [qlo, qhi) of the tile's expand rows (every contributor of a split tile takes
+    // a contiguous share: the LoRA term is linear and rides the split-K reduction)
+    auto mt_range = [&](int u, int& tile, int& qlo, int& qhi) {
+      tile = u / p.k_blocks;
+      const int kb0 = u - tile * p.k_blocks, kb1 = min(p.k_blocks, kb0 + (u_hi - u));
+      int ci = 0, ns = 1;
+      if (CL) {
+        ci = (int)ptx::cluster_ctarank();
+        ns = p.cluster;
+      } else if (!(kb0 == 0 && kb1 == p.k_blocks)) {
+        const long long ts = (long long)tile * p.k_blocks;
+        const int c_first = dec_cta_of(ts, UNITS, GRID), c_last = dec_cta_of(ts + p.k_blocks - 1, UNITS, GRID);
+        ci = cta - c_first;
+        ns = c_last - c_first + 1;
+      }
+      qlo = (int)((long long)G.qtot * ci / ns);
+      qhi = (int)((long long)G.qtot * (ci + 1) / ns);
+      const int n0 = tile * kDecBM, jt = dec_slice_of(p.g, n0);
+      if (n0 >= p.g.e_hi[jt] || n0 + kDecBM <= p.g.e_lo[jt]) qhi = qlo;  // tile outside the expand window
+    };
+    // rows [qa, qa + 64) of the share, this tile's 128 columns, into chunk buffer `buf` (zeros past the window)
+    auto mt_stage = [&](int tile, int qa, int qhi, int buf) {
+      const int n0 = tile * kDecBM, jt = dec_slice_of(p.g, n0);
+      const int lo = p.g.e_lo[jt], hi = p.g.e_hi[jt], ldb = hi - lo;
+      uint16_t* dst = s_Bm + buf * L::kMtRows * kDecBM;
+      const int qb = min(qhi, qa + L::kMtRows), ng = G.ngroups;
+      for (int e = etid; e < L::kMtRows * 16; e += 128) {
+        const int rq = e >> 4, nn = n0 + (e & 15) * 8, q = qa + rq;
+        const bool ok = q < qb && nn >= lo && nn < hi;
+        const __nv_bfloat16* src = p.arena;
+        if (ok) {
+          const int gq = dec_find_group(G.gq0, ng, q);
+          src = p.arena + G.goffB[gq][jt] + (size_t)(q - G.gq0[gq]) * ldb + (nn - lo);
+        }
+        ptx::cp_async_16_zfill(dst + rq * kDecBM + (e & 15) * 8, src, ok);
+      }
+      ptx::cp_async_commit();
+    };
+    bool mt_pre = false;
+    float* s_vm = reinterpret_cast<float*>(smem + L::kVmOff);
+    int vm_slice = -1;  // slice whose v s_vm holds
+    if constexpr (L::kMt) {
+      dec_groups64(G, p.ids, T, p.tab, etid, [] { ptx::named_bar_sync(1, 128); });
+      if (etid == 0) DEC_TRACE(13);
+      if (u_lo < u_hi) {
+        int tile, qlo, qhi;
+        mt_range(u_lo, tile, qlo, qhi);
+        if (qlo < qhi) {
+          mt_stage(tile, qlo, qhi, 0);
+          mt_pre = true;
+        }
+      }
+    }
     if (p.pdl) ptx::pdl_wait();  // X (and v) of the preceding kernel are visible; orders our Y writes
     const int par = PUSH ? *p.peer.parity : 0;
     long long vs_key = -1;       // (slice range, K range) whose v_seg s_vs holds
@@ -527,7 +830,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
 #pragma unroll
       for (int i = 0; i < 16; ++i) lr[i] = 0.f;
       // tensor-core K-local shrink taken by the producer (same rule): v_seg arrives in TMEM with the accumulator
-      const bool tc = CL && LM == 1 && p.tc_shrink && p.lora == 1 && ngroups == 1 && s_grs[0] <= 16 &&
+      const bool tc = L::kTcShrink && LM == 1 && p.tc_shrink && p.lora == 1 && ngroups == 1 && s_grs[0] <= 16 &&
                       jlo == dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
       if constexpr (BN == 16) if (LM == 1 && p.lora == 1 && ngroups > 0 && !tc) {
         // ---- K-local shrink of this segment: v_seg[t][j][k] = s_a sum_{d in seg} X[t][d] A_{a,j}[k][d] -----
@@ -647,23 +950,111 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
                       (whole || (CL ? ptx::cluster_ctarank() == 0
                                     : cta == dec_cta_of((long long)tile * p.k_blocks, UNITS, GRID)));
       if (LM == 2 && p.lora == 3 && ngroups > 0 && tile != cur_tile) stage_B(tile);
+      if constexpr (L::kMt) {
+        // ---- LM 3: s_lr[t][row] = sum over this share's rows q of v[t][k(q)] B_{g(q)}[k(q)][n] (matmul_4 / _6
+        // of a precomputed v; only the rows of token t's own group contribute), B rows double-buffered
+        int tl, qlo, qhi;
+        mt_range(u, tl, qlo, qhi);
+        for (int t = 0; t < T; ++t) s_lr[t * kDecBM + row] = 0.f;
+        const int nchk = (qhi - qlo + L::kMtRows - 1) / L::kMtRows;
+        if (nchk > 0 && !mt_pre) mt_stage(tile, qlo, qhi, 0);
+        mt_pre = false;
+        const int jt = jlo, C = p.g.C, J = p.g.J, Rc = p.g.Rc, ng = G.ngroups;
+        const int vrow = C * Rc;  // s_vm row of a token: its C chunks of Rc
+        const bool use_vm = T * vrow <= L::kVmFloats;
+        if (use_vm && nchk > 0 && vm_slice != jt) {
+          // v of this slice for every token in one round of independent loads (v was written by the preceding
+          // kernel and is read many times per row below)
+          vm_slice = jt;
+          for (int i = etid; i < T * vrow; i += 128) {
+            const int t = i / vrow, r2 = i - t * vrow, c = r2 / Rc, kk = r2 - c * Rc;
+            s_vm[i] = __ldg(p.v + ((size_t)(c * T + t) * J + jt) * Rc + kk);
+          }
+        }
+        if (u == u_lo && etid == 0) DEC_TRACE(14);
+        for (int ch = 0; ch < nchk; ++ch) {
+          if (ch + 1 < nchk) {
+            mt_stage(tile, qlo + (ch + 1) * L::kMtRows, qhi, (ch + 1) & 1);
+            ptx::cp_async_wait_group<1>();
+          } else {
+            ptx::cp_async_wait_group<0>();
+          }
+          ptx::named_bar_sync(1, 128);
+          const int qa = qlo + ch * L::kMtRows, qb = min(qhi, qa + L::kMtRows);
+          const uint16_t* sb = s_Bm + (ch & 1) * L::kMtRows * kDecBM + row;
+          for (int gq = dec_find_group(G.gq0, ng, qa); gq < ng && G.gq0[gq] < qb; ++gq) {
+            const int q0 = G.gq0[gq], re = G.gre[gq];
+            const int k0 = max(qa, q0) - q0, k1 = min(qb, q0 + re) - q0;
+            if (k1 <= k0) continue;
+            const int rc = re / C;
+            const uint16_t* sbg = sb + (q0 - qa) * kDecBM;
+            for (int m = 0; m < G.gcnt[gq]; ++m) {
+              const int t = G.gmem[G.gst[gq] + m];
+              float s4[4] = {0.f, 0.f, 0.f, 0.f};
+              if (use_vm) {
+                const float* vv = s_vm + t * vrow;
+                int k = k0;
+                if (C == 1) {
+                  for (; k + 4 <= k1; k += 4) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) s4[e] = fmaf(vv[k + e], bf16_bits_to_f32(sbg[(k + e) * kDecBM]), s4[e]);
+                  }
+                  for (; k < k1; ++k) s4[0] = fmaf(vv[k], bf16_bits_to_f32(sbg[k * kDecBM]), s4[0]);
+                } else {  // S-LoRA column after the all-gather: rank row k lives in chunk k / (re / C)
+                  for (; k < k1; ++k) {
+                    const int c = k / rc;
+                    s4[k & 3] = fmaf(vv[c * Rc + (k - c * rc)], bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
+                  }
+                }
+              } else if (C == 1) {
+                const float* vv = p.v + ((size_t)t * J + jt) * Rc;
+                int k = k0;
+                for (; k + 4 <= k1; k += 4) {
+                  float vk[4], bk[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    vk[e] = __ldg(vv + k + e);
+                    bk[e] = bf16_bits_to_f32(sbg[(k + e) * kDecBM]);
+                  }
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) s4[e] = fmaf(vk[e], bk[e], s4[e]);
+                }
+                for (; k < k1; ++k) s4[0] = fmaf(__ldg(vv + k), bf16_bits_to_f32(sbg[k * kDecBM]), s4[0]);
+              } else {  // S-LoRA column after the all-gather: rank row k lives in chunk k / (re / C)
+                for (int k = k0; k < k1; ++k) {
+                  const int c = k / rc;
+                  s4[k & 3] = fmaf(__ldg(p.v + ((size_t)(c * T + t) * J + jt) * Rc + (k - c * rc)),
+                                   bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
+                }
+              }
+              s_lr[t * kDecBM + row] += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            }
+          }
+          ptx::named_bar_sync(1, 128);  // chunk buffer (ch & 1) free for chunk ch + 2
+        }
+        if (u == u_lo && etid == 0) DEC_TRACE(15);
+      }
       if (u == u_lo && etid == 0) DEC_TRACE(3);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       if (u == u_lo && etid == 0) DEC_TRACE(4);
       if (tc) {
-        // v_seg (TMEM lanes k < r/N of the shrink accumulator, read by the lane-quarter-0 warp) -> s_vs
+        // v_seg (TMEM lanes k < r/N of the shrink accumulator, read by the lane-quarter-0 warp) -> s_vs.  A CTA
+        // of a stream-K grid owns several segments: every reader of the previous segment's s_vs is done first,
+        // and this tile's B rows replace the previous tile's (each thread stages and reads only its own column)
+        if (tile != cur_tile) stage_B(tile);
+        ptx::named_bar_sync(1, 128);
         if (q4 == 0) {
           const int rs = s_grs[0];
           const float sc = s_gsc[0];
 #pragma unroll
           for (int c0 = 0; c0 < BN; c0 += 16) {
             uint32_t v16[16];
-            ptx::tmem_ld_32x32b_x16(tmem_base + (uint32_t)(L::kVCol + c0), v16);
+            ptx::tmem_ld_32x32b_x16(tmem_base + (uint32_t)(L::kVCol + acc * BN + c0), v16);
             ptx::tmem_ld_wait();
-            if (lane < rs) {
+            if (lane < 16) {  // rows rs..15 are written as zeros (dec_dot16 reads all 16)
 #pragma unroll
-              for (int t = 0; t < 16; ++t) s_vs[(c0 + t) * L::kVsTok + lane] = sc * __uint_as_float(v16[t]);
+              for (int t = 0; t < 16; ++t) s_vs[(c0 + t) * L::kVsTok + lane] = lane < rs ? sc * __uint_as_float(v16[t]) : 0.f;
             }
           }
         }
@@ -687,13 +1078,22 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         ptx::tmem_ld_wait();
         const int tn = min(16, T - c0);  // valid tokens of the chunk
         if (tc) {
+          // this output column's B values of the adapter's rank rows in registers (zero past r/N), then one
+          // 16-term dot per token against its v_seg row (broadcast 16-byte shared loads)
+          float bq[16];
+          const int rs = s_grs[0];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) bq[k] = k < rs ? bf16_bits_to_f32(s_B[k * kDecBM + row]) : 0.f;
           if (BN == 16 && T == 1) {  // straight-line batch-1 path (no 16-way guarded unroll: i-cache)
-            if (s_grp[0] == 0) lr[0] = dec_dot(s_vs, s_B + row, s_grs[0]);
+            if (s_grp[0] == 0) lr[0] = dec_dot16(s_vs, bq);
           } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              lr[i] = (i < tn && s_grp[c0 + i] == 0) ? dec_dot(s_vs + (c0 + i) * L::kVsTok, s_B + row, s_grs[0]) : 0.f;
+              lr[i] = (i < tn && s_grp[c0 + i] == 0) ? dec_dot16(s_vs + (c0 + i) * L::kVsTok, bq) : 0.f;
           }
+        } else if (L::kMt) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) lr[i] = i < tn ? s_lr[(c0 + i) * kDecBM + row] : 0.f;
         } else if (v3) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {

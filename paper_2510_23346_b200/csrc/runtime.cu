@@ -253,6 +253,17 @@ int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids
                   void* ws = nullptr) {
   if (T == 0) return BDLORA_OK;
   const Geom& g = p->g;
+  if (T <= bdl::kDecMaxT && bdl::dec_enabled() && g.K % 8 == 0) {
+    // decode-sized batch: one grid-wide launch, every distinct adapter's A rows read once
+    const int rc = bdl::dec_shrink_launch(g, (const __nv_bfloat16*)X, T, ids, p->d_tab, (const __nv_bfloat16*)p->arena,
+                                          v, p->num_sms, st, g_pdl);
+    if (rc < 0) return fail(BDLORA_E_CUDA, "decode shrink launch: %s", cudaGetErrorString(cudaGetLastError()));
+    if (rc == 0) {
+      count_launch();
+      g_last_src = 1;
+      return BDLORA_OK;
+    }
+  }
   const size_t per_tok = (size_t)g.J * g.Rc;
   for (int c0 = 0; c0 < T; c0 += bdl::kRouteMaxSeg) {
     const int Tc = std::min(T - c0, bdl::kRouteMaxSeg);
@@ -394,6 +405,15 @@ bool decode_klocal_ok(const bdlora_pool* p, int T) {
   return (int64_t)std::min<int64_t>(T, p->d.capacity) * p->rs_max <= bdl::kDecLoraRowsHost;
 }
 
+// Multi-adapter decode (lora 4, any number of adapters, T <= 64): the precomputed v is expanded in the decode
+// kernel's epilogue; every 128-column tile must lie inside one slice (its B rows come from one B_j).
+bool decode_mt_ok(const bdlora_pool* p, int T) {
+  if (T < 1 || T > bdl::kDecMaxT || g_push || !bdl::dec_enabled() || !bdl::dec_eligible(p->g, T)) return false;
+  for (int j = 0; j < p->g.J; ++j)
+    if (p->g.col0[j] % 128 || p->g.e_lo[j] % 128) return false;
+  return true;
+}
+
 int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W, const int32_t* ids, const float* v,
                        void* Y, void* ws, cudaStream_t st) {
   const int pdl = g_pdl;
@@ -402,8 +422,13 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
     // v precomputed: staged-B expand (mode 3) when the batch's distinct adapters fit the kernel's rank-row
     // capacity in the worst case, else the per-output gather (mode 2)
     const bool staged = (int64_t)std::min<int64_t>(T, p->d.capacity) * p->re_max <= bdl::kDecLoraRowsHost;
-    if (T <= 16 || (p->d.capacity == 1 && staged)) {  // 17..64 tokens: one-adapter pools only (BN = 64 tiles)
-      const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, staged ? 3 : 2);
+    const bool mt = decode_mt_ok(p, T);
+    int mode = 0;
+    if (staged && (T <= 16 || p->d.capacity == 1)) mode = 3;  // 17..64 tokens: one-adapter pools (BN = 64)
+    else if (mt) mode = 4;
+    else if (T <= 16) mode = 2;
+    if (mode) {
+      const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, mode);
       if (rc >= 0) return rc;
     }
   }
@@ -425,11 +450,14 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
 
 float* ws_v(const bdlora_pool* p, void* ws, int64_t T) { return (float*)((char*)ws + ws_layout(p, T).off_v); }
 
+const char* sharding_name(int sharding) {
+  return sharding == BDLORA_SHARD_BD ? "BD" : sharding == BDLORA_SHARD_SLORA ? "SLORA" : sharding == BDLORA_SHARD_NFS ? "NFS" : "?";
+}
+
 int require_mode(const bdlora_pool* p, int parallel, int sharding, const char* fn) {
   if (p->d.parallel != parallel || p->d.sharding != sharding)
     return fail(BDLORA_E_MODE, "%s: pool is %s+%s, expected %s+%s", fn, p->d.parallel == BDLORA_COLUMN ? "COLUMN" : "ROW",
-                p->d.sharding == BDLORA_SHARD_BD ? "BD" : "SLORA", parallel == BDLORA_COLUMN ? "COLUMN" : "ROW",
-                sharding == BDLORA_SHARD_BD ? "BD" : "SLORA");
+                sharding_name(p->d.sharding), parallel == BDLORA_COLUMN ? "COLUMN" : "ROW", sharding_name(sharding));
   return BDLORA_OK;
 }
 
@@ -1019,6 +1047,19 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
     // decode: ONE lean kernel -- base GEMM on the tensor cores, K-local LoRA shrink + expand in its epilogue
     const int rc = launch_decode(p, X, (int)T, W, ids, nullptr, Y, ws, st, 1);
     if (rc >= 0) return rc;
+  }
+  if (p->g.C == 1 && decode_mt_ok(p, (int)T)) {
+    // decode batch over many adapters: grid-wide shrink (each distinct adapter's A rows read once), then the
+    // decode kernel expands v in its epilogue (programmatic dependent launch: the weights stream meanwhile)
+    const int rs = bdl::dec_shrink_launch(p->g, (const __nv_bfloat16*)X, (int)T, ids, p->d_tab,
+                                          (const __nv_bfloat16*)p->arena, v, p->num_sms, st, g_pdl);
+    if (rs < 0) return fail(BDLORA_E_CUDA, "decode shrink launch: %s", cudaGetErrorString(cudaGetLastError()));
+    if (rs == 0) {
+      count_launch();
+      const int rc = launch_decode(p, X, (int)T, W, ids, v, Y, ws, st, 4);
+      if (rc >= 0) return rc;
+      return launch_base_expand(p, X, (int)T, W, ids, v, Y, ws, st);
+    }
   }
   if (bdl::umma_eligible(p->g, (int)T) && T <= fused_max_t()) {
     // decode: ONE kernel -- the LoRA shrink runs inside it (K-local on the tensor cores for a single

@@ -247,3 +247,111 @@ def test_decode_bn64_nfs_and_slora(dev, T):
         _assert_tol(_np(Y), _ref(case, i), f"slora v-mode T={T} rank {i}")
     for p in pools:
         p.close()
+
+
+# ----------------------------------------------------------------------------- many adapters, T <= 64 (lora 4)
+# configs[4]-shaped batches: more distinct adapters than the K-local capacity -> one grid-wide shrink launch
+# (dec_shrink_kernel, every distinct adapter's A rows read once) + the decode kernel expanding the precomputed v
+# in its epilogue, each split contributor taking a share of the tile's rank rows through 64-row B chunks.
+
+MT_COL = synth.Projection("qkv_s", "column", 1024, (1024, 256, 256))
+MT_ROW = synth.Projection("down_s", "row", 2048, (1024,))
+
+
+def _mt_ids(seed, T, n_ad):
+    rng = synth.rng_for(seed, 2)
+    ids = rng.integers(0, n_ad, T).astype(np.int32)
+    ids[rng.random(T) < 0.1] = -1
+    return ids
+
+
+@pytest.mark.parametrize("T", [3, 17, 64])
+@pytest.mark.parametrize("proj,n", [(MT_COL, 1), (MT_COL, 2), (MT_ROW, 2), (MT_ROW, 8)])
+def test_decode_multi_adapter_vs_oracle(dev, T, proj, n):
+    """12 resident adapters of ranks 8..128 (mixed), uniform ids with -1 tokens: BN = 64 asserted, every rank of
+    the batch's groups through the chunked expand, first and last tp_rank."""
+    ranks = [[8, 16, 32, 64, 128][a % 5] for a in range(12)]
+    case = H.make_case(6000 + T + 10 * n + len(proj.d_out), proj, "bd", n, T, ranks=ranks, ids=_mt_ids(6000 + T, T, 12))
+    for i in sorted({0, n - 1}):
+        y, info = _run(case, i, dev)
+        assert info["bn"] == 64, info
+        _assert_tol(y, _ref(case, i), f"{proj.name} N={n} T={T} rank {i} grid {info['grid']} cluster {info['cluster']}")
+
+
+@pytest.mark.parametrize("T", [8, 64])
+def test_decode_multi_adapter_many_chunks(dev, T):
+    """24 adapters up to rank 128 at N = 4 (about 600 expand rows per tile: several 64-row B chunks per
+    contributor), all distinct ids at T = 8 and uniform ids at T = 64."""
+    proj = synth.Projection("qkv_m", "column", 4096, (2048, 512, 512))
+    ranks = [[8, 16, 32, 64, 128][a % 5] for a in range(24)]
+    ids = np.arange(T, dtype=np.int32) * 3 % 24 if T == 8 else _mt_ids(6100, T, 24)
+    case = H.make_case(6100 + T, proj, "bd", 4, T, ranks=ranks, ids=ids)
+    for i in (0, 3):
+        y, info = _run(case, i, dev)
+        assert info["bn"] == 64, info
+        _assert_tol(y, _ref(case, i), f"many chunks T={T} rank {i}")
+
+
+@pytest.mark.parametrize("T", [5, 64])
+def test_decode_multi_adapter_integer_bit_exact(dev, T):
+    """P10 through the multi-adapter path: integer inputs, power-of-two scales, per-adapter B signatures --
+    routing, the shrink and the share-split expand are exact, so the output is bit-identical."""
+    ranks = [8, 16, 32, 8, 16, 32, 64, 8, 16, 32]
+    for proj, n in ((MT_COL, 2), (MT_ROW, 4)):
+        case = H.make_case(6200 + T + n, proj, "bd", n, T, ranks=ranks, integer=True, ids=_mt_ids(6200 + T, T, 10))
+        for i in sorted({0, n - 1}):
+            y, info = _run(case, i, dev)
+            assert info["bn"] == 64, info
+            ref = ol.bf16_round(_ref(case, i))
+            assert np.array_equal(y, ref), f"{proj.name} N={n} T={T} rank {i}: {np.count_nonzero(y != ref)} mismatches"
+
+
+@pytest.mark.parametrize("T", [9, 48])
+def test_decode_multi_adapter_slora_expand(dev, T):
+    """S-LoRA column at N = 2 with 8 mixed-rank adapters: the grid-wide shrink writes each rank's v chunk, the
+    all-gather is emulated by concatenation, bdlora_base_expand expands C = N chunks of v (lora 4)."""
+    import torch
+
+    import paper_2510_23346_b200 as bd
+
+    n = 2
+    ranks = [8, 16, 32, 64, 16, 8, 32, 64]
+    case = H.make_case(6300 + T, MT_COL, "slora", n, T, ranks=ranks, ids=_mt_ids(6300 + T, T, 8))
+    pools = [H.make_pool(case, i) for i in range(n)]
+    vs = []
+    for i, p in enumerate(pools):
+        X, W, idt = H.device_inputs(case, i, dev)
+        v = torch.zeros(bd.bdlora_v_elems(p, T), dtype=torch.float32, device=dev)
+        bd.bdlora_lora_shrink(p, X, idt, v, bd.make_workspace(p, T))
+        vs.append(v)
+    vg = torch.cat(vs)
+    for i, p in enumerate(pools):
+        X, W, idt = H.device_inputs(case, i, dev)
+        Y = torch.empty(T, p.m_loc, dtype=torch.bfloat16, device=dev)
+        bd.bdlora_base_expand(p, X, W, idt, vg, Y, bd.make_workspace(p, T))
+        info = bd.bdlora_last_launch_info()
+        assert info["kind"] == 3 and info["bn"] == 64, info
+        torch.cuda.synchronize()
+        _assert_tol(_np(Y), _ref(case, i), f"slora lora-4 T={T} rank {i}")
+    for p in pools:
+        p.close()
+
+
+@pytest.mark.parametrize("T", [24, 64])
+@pytest.mark.parametrize("integer", [False, True])
+def test_decode_bn64_streamk_slices(dev, T, integer):
+    """64-token tiles of a one-adapter pool on a stream-K grid (160 tiles > #SM: no cluster, CTAs owning parts of
+    two tiles, one of them at the gate | up slice boundary): the tensor-core K-local shrink takes each stage's A
+    box from its own tile's slice and double-buffers v_seg with the accumulator."""
+    proj = synth.Projection("gu_wide", "column", 256, (10240, 10240))
+    rng = synth.rng_for(6400 + T, 1)
+    ids = np.where(rng.random(T) < 0.2, -1, 0).astype(np.int32)
+    case = H.make_case(6400 + T + integer, proj, "bd", 1, T, ranks=[16], ids=ids, integer=integer)
+    y, info = _run(case, 0, dev)
+    assert info["bn"] == 64 and info["cluster"] == 1, info
+    ref = _ref(case, 0)
+    if integer:
+        ref = ol.bf16_round(ref)
+        assert np.array_equal(y, ref), f"T={T}: {np.count_nonzero(y != ref)} mismatches"
+    else:
+        _assert_tol(y, ref, f"stream-K bn64 T={T}")
