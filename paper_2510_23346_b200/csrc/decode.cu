@@ -159,7 +159,9 @@ int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* i
                       const __nv_bfloat16* arena, float* v, int num_sms, cudaStream_t st, int pdl) {
   if (T < 1 || T > kDecMaxT) return 1;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(std::max(1, 2 * num_sms));  // two items per CTA, grid-stride; leaves room for the GEMM's CTAs
+  // one item (A row) per CTA and pass, grid-stride: four CTAs per SM resident (<= 128 registers), so that
+  // most batches take one pass; the GEMM's CTAs still fit beside them (no shared memory here but the tables)
+  cfg.gridDim = dim3(std::max(1, 4 * num_sms));
   cfg.blockDim = dim3(kDecShrinkThreads);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -167,7 +169,8 @@ int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* i
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, dec_shrink_kernel, X, T, ids, tab, arena, g, v, pdl) == cudaSuccess ? 0 : -1;
+  static const int late = env_int("BDLORA_SHRINK_LATE_TRIGGER", 0);
+  return cudaLaunchKernelEx(&cfg, dec_shrink_kernel, X, T, ids, tab, arena, g, v, pdl, late) == cudaSuccess ? 0 : -1;
 }
 
 size_t dec_counter_bytes() { return sizeof(int) * kDecMaxGrid; }

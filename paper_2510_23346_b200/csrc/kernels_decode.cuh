@@ -112,28 +112,31 @@ struct DecSmem {
   // offset q0  [80,96) member masks  [96] n_groups  [97] rows total ; floats [128,144) group scale ;
   // long long [160 + 2*(g*3 + j)) group A / B offsets per slice (as int pairs)
   // ... [960, 1024) group of each of up to 64 tokens.  LM 3: a DecGroups.
-  static constexpr int kMiscBytes = kMt ? 8192 : 4096;
-  static_assert(!kMt || sizeof(DecGroups) <= kMiscBytes, "group tables");
+  static constexpr int kMiscBytes = kMt ? 12288 : 4096;
+  static constexpr int kMtListOff = 8192;  // LM 3: per chunk buffer and warp, the tokens whose group meets the chunk
+  static_assert(!kMt || sizeof(DecGroups) <= kMtListOff, "group tables");
   // v_seg: BN = 16: [16 tokens][3 slices][32] fp32; BN = 64 (one adapter, one slice per tile): [64][32]
   static constexpr int kVsTok = BN == 16 ? 3 * kDecLoraRows : kDecLoraRows;
   static constexpr int kVsOff = kMiscOff + kMiscBytes;
   static constexpr int kVsBytes = kMt ? 0 : BN * kVsTok * 4;
-  // B rows of the tile's columns: [32][128] bf16; LM 3: two 64-row chunk buffers (cp.async double buffering)
+  // B rows of the tile's columns: [32][128] bf16; LM 3: two 96-row chunk buffers (cp.async double buffering;
+  // both issued before the programmatic-dependency wait, so a share of <= 192 rows is in flight in one shot)
   static constexpr int kBOff = kVsOff + kVsBytes;
-  static constexpr int kMtRows = 64;
+  static constexpr int kMtRows = 96;
   static constexpr int kBBytes = kMt ? 2 * kMtRows * kDecBM * 2 : kDecLoraRows * kDecBM * 2;
-  // LM 3: the tile's LoRA terms [64 tokens][128 columns] fp32 (a thread owns one column)
+  // (LM 3 keeps the tile's LoRA terms in TMEM columns [kLrCol, kLrCol + 64): thread = TMEM lane = column)
   static constexpr int kLrOff = kBOff + kBBytes;
-  static constexpr int kLrBytes = kMt ? 64 * kDecBM * 4 : 0;
+  static constexpr int kLrBytes = 0;
+  static constexpr int kLrCol = 2 * BN;
   // LM 3: v of the tile's slice staged once, [T][C * Rc] fp32 (when it fits)
   static constexpr int kVmOff = kLrOff + kLrBytes;
-  static constexpr int kVmFloats = kMt ? 4096 : 0;
+  static constexpr int kVmFloats = kMt ? 8192 : 0;
   // cluster split-K: [s][ceil(128/s)][16] fp32 partial slots the peers push into (<= (128 + s) x 16 floats)
   static constexpr int kSlotOff = kVmOff + kVmFloats * 4;
   static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * BN * 4 : 0;
   static constexpr int kBytes = kSlotOff + kSlotBytes + 1024;   // + 1024-B alignment slack
   static constexpr int kVCol = 2 * BN;                          // TMEM: [acc 0 | acc 1 | v_seg 0 | v_seg 1]
-  static constexpr int kTmemCols = BN == 16 ? (CL ? 64 : 32) : (kMt ? 128 : 256);
+  static constexpr int kTmemCols = BN == 16 ? (CL ? 64 : 32) : 256;
   static_assert(S > 5 || BN > 16 || kBytes <= 113 * 1024, "two CTAs per SM");
   static_assert(kBytes <= 227 * 1024, "shared memory per CTA");
 };
@@ -234,107 +237,96 @@ __device__ __forceinline__ int dec_find_group(const int* pre, int ng, int q) {
 
 // Multi-adapter LoRA shrink of a decode batch (matmul_3 / matmul_5 for T <= 64 tokens over many adapters,
 // P:287-288):  v[t][j][k] = s_a(t) X[t] . A_{a(t),j}[k]  (fp32, scaled; layout [T][J][Rc]).
-// Work item = one A row (group g, slice j, rank row k): read from HBM exactly once, dotted with every member
-// token of the group.  Four warps share an item (one K quarter each, 16-byte loads, 8 in flight per lane),
-// fixed-order reduction (deterministic).  Launched before the decode GEMM with programmatic dependent launch:
-// the GEMM streams its weights while this runs.
-constexpr int kDecShrinkThreads = 256;
-__global__ void __launch_bounds__(kDecShrinkThreads) dec_shrink_kernel(const __nv_bfloat16* __restrict__ X, int T,
-                                                                       const int* __restrict__ ids,
-                                                                       const SlotEntry* __restrict__ tab,
-                                                                       const __nv_bfloat16* __restrict__ arena, Geom g,
-                                                                       float* __restrict__ v, int pdl) {
-  __shared__ DecGroups G;
-  __shared__ float s_red[2][4][4];
+// Work item = one (token, slice, rank row) dot product of length K: four warps share an item (one K quarter
+// each, 8 A + 8 X 16-byte loads in flight per lane), fixed-order reduction (deterministic).  Tokens of one
+// adapter read the same A rows (L2 hits after the first).  Launched before the decode GEMM with programmatic
+// dependent launch: the GEMM streams its weights (and stages its B rows) while this runs.
+constexpr int kDecShrinkThreads = 128;
+__global__ void __launch_bounds__(kDecShrinkThreads, 4) dec_shrink_kernel(const __nv_bfloat16* __restrict__ X, int T,
+                                                                          const int* __restrict__ ids,
+                                                                          const SlotEntry* __restrict__ tab,
+                                                                          const __nv_bfloat16* __restrict__ arena,
+                                                                          Geom g, float* __restrict__ v, int pdl,
+                                                                          int late_trigger) {
+  __shared__ int s_pre[65];               // exclusive prefix over tokens of J * rs(a(t)) (items)
+  __shared__ int s_rs[64];
+  __shared__ float s_sc[64];
+  __shared__ long long s_offA[64][kMaxSlices];
+  __shared__ int s_wtot;
+  __shared__ float s_red[4];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  dec_groups64(G, ids, T, tab, tid, [] { __syncthreads(); });
-  if (tid == 0) ptx::pdl_launch_dependents();  // the GEMM may start streaming its weights
-  if (pdl) ptx::pdl_wait();                    // X is written by the preceding kernel
-  const int J = g.J, K = g.K, ng = G.ngroups;
-  const int items = J * G.ptot;
-  const int half = warp >> 2, quarter = warp & 3;  // two items per CTA, four warps per item
-  const int nch = K >> 3;                          // 16-byte chunks of a row
-  const int c_lo = (nch * quarter) >> 2, c_hi = (nch * (quarter + 1)) >> 2;
-  for (int it0 = blockIdx.x * 2; it0 < items; it0 += gridDim.x * 2) {
-    const int it = it0 + half;
-    const bool valid = it < items;
-    int gi = 0, j = 0, k = 0;
-    if (valid) {
-      // item -> (group, slice, row): groups own J * rs consecutive items, slice-major inside a group
-      int lo = 0, hi = ng - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (J * G.gp0[mid] <= it) lo = mid;
-        else hi = mid - 1;
-      }
-      gi = lo;
-      const int r = it - J * G.gp0[gi];
-      j = r / G.grs[gi];
-      k = r - j * G.grs[gi];
+  const int J = g.J, K = g.K;
+  if (tid < 64) {  // ids and the slot table are not written by the preceding kernel (bdlora_set_pdl contract)
+    const int id = tid < T ? __ldg(ids + tid) : -1;
+    int rs = 0;
+    if (id >= 0) {
+      const SlotEntry e = tab[id];
+      rs = e.rs;
+      s_sc[tid] = e.scale;
+#pragma unroll
+      for (int j = 0; j < kMaxSlices; ++j) s_offA[tid][j] = e.offA[j];
     }
-    const int cnt = valid ? G.gcnt[gi] : 0;
-    const __nv_bfloat16* Arow = arena + G.goffA[gi][j] + (size_t)k * K;
-    for (int tb = 0; tb < 64; tb += 4) {  // member tokens, 4 per pass (block-uniform trip count)
-      const int ntb = __syncthreads_or(tb < cnt);
-      if (!ntb) break;
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      int tok[4];
+    s_rs[tid] = rs;
+    int incl = J * rs;
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) tok[qq] = (tb + qq < cnt) ? G.gmem[G.gst[gi] + tb + qq] : -1;
-      if (tb < cnt) {
-        // blocks of 8 chunks per lane (256 per warp): the 8 A loads, then 2 tokens' 16 X loads, all in flight
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (tid == 31) s_wtot = incl;
+    s_pre[tid + 1] = incl;  // warp-local inclusive; warp 1 adds warp 0's total below
+  }
+  __syncthreads();
+  if (tid >= 32 && tid < 64) s_pre[tid + 1] += s_wtot;
+  if (tid == 0) s_pre[0] = 0;
+  __syncthreads();
+  // the GEMM may start streaming its weights -- unless its CTAs (one per SM, ~226 KB of shared memory) would
+  // crowd this grid out of the SMs (late_trigger: launched once this CTA's items are done)
+  if (tid == 0 && !late_trigger) ptx::pdl_launch_dependents();
+  if (pdl) ptx::pdl_wait();                    // X is written by the preceding kernel
+  const int items = s_pre[64];
+  const int nch = K >> 3;  // 16-byte chunks of a row
+  const int c_lo = (nch * warp) >> 2, c_hi = (nch * (warp + 1)) >> 2;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int lo = 0, hi = 63;  // token: largest t with s_pre[t] <= it
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= it) lo = mid;
+      else hi = mid - 1;
+    }
+    const int t = lo, rs = s_rs[t];
+    const int r = it - s_pre[t], j = r / rs, k = r - j * rs;
+    const __nv_bfloat16* Arow = arena + s_offA[t][j] + (size_t)k * K;
+    const __nv_bfloat16* Xrow = X + (size_t)t * K;
+    float acc = 0.f, acc2 = 0.f;
 #pragma unroll 1
-        for (int cb = c_lo; cb < c_hi; cb += 256) {
-          uint4 av[8];
+    for (int cb = c_lo; cb < c_hi; cb += 256) {  // 8 chunks per lane per block (one block at K = 8192)
+      uint4 av[8], xv[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int cc = cb + lane + 32 * u;
-            av[u] = cc < c_hi ? ld_cached_u4(Arow + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
-          }
+      for (int u = 0; u < 8; ++u) {
+        const int cc = cb + lane + 32 * u;
+        av[u] = cc < c_hi ? ld_cached_u4(Arow + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
+        xv[u] = cc < c_hi ? ld_cached_u4(Xrow + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
+      }
 #pragma unroll
-          for (int qp = 0; qp < 4; qp += 2) {
-            if (tb + qp < cnt) {
-              const __nv_bfloat16* xr0 = X + (size_t)tok[qp] * K;
-              const __nv_bfloat16* xr1 = X + (size_t)(tok[qp + 1] >= 0 ? tok[qp + 1] : tok[qp]) * K;
-              uint4 x0[8], x1[8];
+      for (int u = 0; u < 8; ++u) {
+        float af[8], xf[8];
+        bf16x8_to_f32(av[u], af);
+        bf16x8_to_f32(xv[u], xf);
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int cc = cb + lane + 32 * u;
-                x0[u] = cc < c_hi ? ld_cached_u4(xr0 + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
-                x1[u] = cc < c_hi ? ld_cached_u4(xr1 + (size_t)cc * 8) : make_uint4(0u, 0u, 0u, 0u);
-              }
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                float af[8], f0[8], f1[8];
-                bf16x8_to_f32(av[u], af);
-                bf16x8_to_f32(x0[u], f0);
-                bf16x8_to_f32(x1[u], f1);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  acc[qp] = fmaf(af[e], f0[e], acc[qp]);
-                  acc[qp + 1] = fmaf(af[e], f1[e], acc[qp + 1]);
-                }
-              }
-            }
-          }
+        for (int e = 0; e < 8; e += 2) {
+          acc = fmaf(af[e], xf[e], acc);
+          acc2 = fmaf(af[e + 1], xf[e + 1], acc2);
         }
       }
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) acc[qq] = warp_sum(acc[qq]);
-      if (lane == 0) {
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) s_red[half][quarter][qq] = acc[qq];
-      }
-      __syncthreads();
-      const int tq = lane == 0 ? tok[0] : lane == 1 ? tok[1] : lane == 2 ? tok[2] : tok[3];
-      if (quarter == 0 && lane < 4 && tq >= 0) {
-        const int qq = lane;
-        const float sum = (s_red[half][0][qq] + s_red[half][1][qq]) + (s_red[half][2][qq] + s_red[half][3][qq]);
-        v[((size_t)tq * J + j) * g.Rc + k] = G.gsc[gi] * sum;
-      }
-      __syncthreads();
     }
+    const float ws = warp_sum(acc + acc2);
+    if (lane == 0) s_red[warp] = ws;
+    __syncthreads();
+    if (tid == 0) v[((size_t)t * J + j) * g.Rc + k] = s_sc[t] * ((s_red[0] + s_red[1]) + (s_red[2] + s_red[3]));
+    __syncthreads();
   }
+  if (tid == 0 && late_trigger) ptx::pdl_launch_dependents();
 }
 
 __device__ __forceinline__ int dec_u_lo(long long c, int units, int grid) { return (int)(c * units / grid); }
@@ -757,7 +749,6 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
     // ---- LM 3: adapter groups of the batch; the first segment's first chunk of B rows staged before the wait
     DecGroups& G = *reinterpret_cast<DecGroups*>(mi);
     uint16_t* s_Bm = reinterpret_cast<uint16_t*>(smem + L::kBOff);
-    float* s_lr = reinterpret_cast<float*>(smem + L::kLrOff);
     // this contributor's share [qlo, qhi) of the tile's expand rows (every contributor of a split tile takes
     // a contiguous share: the LoRA term is linear and rides the split-K reduction)
     auto mt_range = [&](int u, int& tile, int& qlo, int& qhi) {
@@ -795,6 +786,25 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         ptx::cp_async_16_zfill(dst + rq * kDecBM + (e & 15) * 8, src, ok);
       }
       ptx::cp_async_commit();
+      // the chunk's token list: (token, first expand row of its group inside the chunk, rows, chunk row offset)
+      // for every token whose group's rows meet [qa, qb) -- built by the first two epilogue warps
+      if (etid < 64) {
+        int klo = 0, nr = 0, off = 0;
+        const int gt = etid < T ? G.grp[etid] : -1;
+        if (gt >= 0) {
+          const int q0 = G.gq0[gt], qlo2 = max(qa, q0), qhi2 = min(qb, q0 + G.gre[gt]);
+          if (qlo2 < qhi2) {
+            klo = qlo2 - q0;
+            nr = qhi2 - qlo2;
+            off = qlo2 - qa;
+          }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, nr > 0);
+        const int w = etid >> 5;
+        int4* lst = reinterpret_cast<int4*>(reinterpret_cast<uint8_t*>(mi) + L::kMtListOff) + (buf * 2 + w) * 32;
+        if (nr > 0) lst[__popc(m & ((1u << (etid & 31)) - 1u))] = make_int4(etid, klo, nr, off);
+        if ((etid & 31) == 0) mi[(L::kMtListOff + 2 * 2 * 32 * 16) / 4 + buf * 2 + w] = __popc(m);
+      }
     };
     bool mt_pre = false;
     float* s_vm = reinterpret_cast<float*>(smem + L::kVmOff);
@@ -807,6 +817,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         mt_range(u_lo, tile, qlo, qhi);
         if (qlo < qhi) {
           mt_stage(tile, qlo, qhi, 0);
+          if (qhi - qlo > L::kMtRows) mt_stage(tile, qlo + L::kMtRows, qhi, 1);
           mt_pre = true;
         }
       }
@@ -955,9 +966,15 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         // of a precomputed v; only the rows of token t's own group contribute), B rows double-buffered
         int tl, qlo, qhi;
         mt_range(u, tl, qlo, qhi);
-        for (int t = 0; t < T; ++t) s_lr[t * kDecBM + row] = 0.f;
+        // this tile's LoRA terms accumulate in TMEM columns [kLrCol, kLrCol + T) of this warp's lane quarter
+        const uint32_t lr_t = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)L::kLrCol;
+        for (int c0 = 0; c0 < T; c0 += 16) ptx::tmem_st_zero_32x32b_x16(lr_t + c0);
+        ptx::tmem_st_wait();
         const int nchk = (qhi - qlo + L::kMtRows - 1) / L::kMtRows;
-        if (nchk > 0 && !mt_pre) mt_stage(tile, qlo, qhi, 0);
+        if (!mt_pre) {
+          if (nchk > 0) mt_stage(tile, qlo, qhi, 0);
+          if (nchk > 1) mt_stage(tile, qlo + L::kMtRows, qhi, 1);
+        }
         mt_pre = false;
         const int jt = jlo, C = p.g.C, J = p.g.J, Rc = p.g.Rc, ng = G.ngroups;
         const int vrow = C * Rc;  // s_vm row of a token: its C chunks of Rc
@@ -973,64 +990,53 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         }
         if (u == u_lo && etid == 0) DEC_TRACE(14);
         for (int ch = 0; ch < nchk; ++ch) {
-          if (ch + 1 < nchk) {
-            mt_stage(tile, qlo + (ch + 1) * L::kMtRows, qhi, (ch + 1) & 1);
-            ptx::cp_async_wait_group<1>();
-          } else {
-            ptx::cp_async_wait_group<0>();
-          }
+          // chunks ch and ch + 1 are in flight (two groups): wait for the older one
+          if (ch + 1 < nchk) ptx::cp_async_wait_group<1>();
+          else ptx::cp_async_wait_group<0>();
           ptx::named_bar_sync(1, 128);
           const int qa = qlo + ch * L::kMtRows, qb = min(qhi, qa + L::kMtRows);
           const uint16_t* sb = s_Bm + (ch & 1) * L::kMtRows * kDecBM + row;
-          for (int gq = dec_find_group(G.gq0, ng, qa); gq < ng && G.gq0[gq] < qb; ++gq) {
-            const int q0 = G.gq0[gq], re = G.gre[gq];
-            const int k0 = max(qa, q0) - q0, k1 = min(qb, q0 + re) - q0;
-            if (k1 <= k0) continue;
-            const int rc = re / C;
-            const uint16_t* sbg = sb + (q0 - qa) * kDecBM;
-            for (int m = 0; m < G.gcnt[gq]; ++m) {
-              const int t = G.gmem[G.gst[gq] + m];
+          const int4* lst = reinterpret_cast<const int4*>(reinterpret_cast<const uint8_t*>(mi) + L::kMtListOff);
+          const int* lcnt = mi + (L::kMtListOff + 2 * 2 * 32 * 16) / 4;
+#pragma unroll 1
+          for (int w = 0; w < 2; ++w) {
+            const int nl = lcnt[(ch & 1) * 2 + w];
+#pragma unroll 1
+            for (int e = 0; e < nl; ++e) {
+              const int4 en = lst[((ch & 1) * 2 + w) * 32 + e];
+              const int t = en.x, klo = en.y, nr = en.z;
+              const uint16_t* sbg = sb + en.w * kDecBM;
+              // the token's running LoRA term: loaded now, waited for after the dot (a token appears once per
+              // chunk, so no store of this chunk is pending on its column)
+              const uint32_t ta = lr_t + (uint32_t)t;
+              const uint32_t lr_old = ptx::tmem_ld_32x32b_x1(ta);
               float s4[4] = {0.f, 0.f, 0.f, 0.f};
-              if (use_vm) {
-                const float* vv = s_vm + t * vrow;
-                int k = k0;
-                if (C == 1) {
-                  for (; k + 4 <= k1; k += 4) {
+              if (use_vm && C == 1) {
+                const float* vv = s_vm + t * vrow + klo;
+                int k = 0;
+                for (; k + 4 <= nr; k += 4) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) s4[e] = fmaf(vv[k + e], bf16_bits_to_f32(sbg[(k + e) * kDecBM]), s4[e]);
-                  }
-                  for (; k < k1; ++k) s4[0] = fmaf(vv[k], bf16_bits_to_f32(sbg[k * kDecBM]), s4[0]);
-                } else {  // S-LoRA column after the all-gather: rank row k lives in chunk k / (re / C)
-                  for (; k < k1; ++k) {
-                    const int c = k / rc;
-                    s4[k & 3] = fmaf(vv[c * Rc + (k - c * rc)], bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
-                  }
+                  for (int q = 0; q < 4; ++q) s4[q] = fmaf(vv[k + q], bf16_bits_to_f32(sbg[(k + q) * kDecBM]), s4[q]);
                 }
-              } else if (C == 1) {
-                const float* vv = p.v + ((size_t)t * J + jt) * Rc;
-                int k = k0;
-                for (; k + 4 <= k1; k += 4) {
-                  float vk[4], bk[4];
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    vk[e] = __ldg(vv + k + e);
-                    bk[e] = bf16_bits_to_f32(sbg[(k + e) * kDecBM]);
-                  }
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) s4[e] = fmaf(vk[e], bk[e], s4[e]);
-                }
-                for (; k < k1; ++k) s4[0] = fmaf(__ldg(vv + k), bf16_bits_to_f32(sbg[k * kDecBM]), s4[0]);
-              } else {  // S-LoRA column after the all-gather: rank row k lives in chunk k / (re / C)
-                for (int k = k0; k < k1; ++k) {
-                  const int c = k / rc;
-                  s4[k & 3] = fmaf(__ldg(p.v + ((size_t)(c * T + t) * J + jt) * Rc + (k - c * rc)),
-                                   bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
+                for (; k < nr; ++k) s4[k & 3] = fmaf(vv[k], bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
+              } else {
+                // generic: v from shared memory or global; S-LoRA column after the all-gather keeps rank row k
+                // in chunk k / (re / C)
+                const int rc = G.gre[G.grp[t]] / C;
+                for (int k = 0; k < nr; ++k) {
+                  const int kk = klo + k, c = kk / rc, kr = kk - c * rc;
+                  const float vk = use_vm ? s_vm[t * vrow + c * Rc + kr]
+                                          : __ldg(p.v + ((size_t)(c * T + t) * J + jt) * Rc + kr);
+                  s4[k & 3] = fmaf(vk, bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
                 }
               }
-              s_lr[t * kDecBM + row] += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+              ptx::tmem_ld_wait();  // warp-uniform list: whole-warp TMEM access
+              ptx::tmem_st_32x32b_x1(ta, __float_as_uint(__uint_as_float(lr_old) + ((s4[0] + s4[1]) + (s4[2] + s4[3]))));
             }
           }
+          ptx::tmem_st_wait();  // this chunk's terms are in TMEM before the next chunk reloads a column
           ptx::named_bar_sync(1, 128);  // chunk buffer (ch & 1) free for chunk ch + 2
+          if (ch + 2 < nchk) mt_stage(tile, qlo + (ch + 2) * L::kMtRows, qhi, ch & 1);
         }
         if (u == u_lo && etid == 0) DEC_TRACE(15);
       }
@@ -1092,8 +1098,11 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
               lr[i] = (i < tn && s_grp[c0 + i] == 0) ? dec_dot16(s_vs + (c0 + i) * L::kVsTok, bq) : 0.f;
           }
         } else if (L::kMt) {
+          uint32_t l16[16];
+          ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(L::kLrCol + c0), l16);
+          ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) lr[i] = i < tn ? s_lr[(c0 + i) * kDecBM + row] : 0.f;
+          for (int i = 0; i < 16; ++i) lr[i] = i < tn ? __uint_as_float(l16[i]) : 0.f;
         } else if (v3) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {

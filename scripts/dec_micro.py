@@ -64,7 +64,10 @@ def run(M, K, T, rank):
     print(f"M={M} K={K} T={T} r={rank}: {us:.2f} us/launch ({gb / (us * 1e-6):.0f} GB/s)  info={info}")
     print(f"   CTAs on distinct SMs {np.count_nonzero(per_sm)} (max per SM {per_sm.max()})")
     for k, nm in [(0, "entry"), (1, "ring0 issued"), (2, "first mma"), (3, "epi pre-wait"), (4, "acc ready"),
-                  (7, "epi end"), (8, "producer end")]:
+                  (9, "tc v read"), (11, "peers started"), (12, "pushed"), (6, "reduced"), (7, "epi end"),
+                  (8, "producer end")]:
+        if (t[:, k] <= 0).all():
+            continue
         c = rel(k)
         print(f"   {nm:14s} min {c.min():7.2f} med {np.median(c):7.2f} max {c.max():7.2f} us")
     end = rel(7)
