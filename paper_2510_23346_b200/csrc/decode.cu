@@ -161,7 +161,8 @@ int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* i
   cudaLaunchConfig_t cfg = {};
   // one item (A row) per CTA and pass, grid-stride: four CTAs per SM resident (<= 128 registers), so that
   // most batches take one pass; the GEMM's CTAs still fit beside them (no shared memory here but the tables)
-  cfg.gridDim = dim3(std::max(1, 4 * num_sms));
+  static const int per_sm = std::max(1, env_int("BDLORA_SHRINK_CTAS_PER_SM", 4));
+  cfg.gridDim = dim3(std::max(1, per_sm * num_sms));
   cfg.blockDim = dim3(kDecShrinkThreads);
   cfg.stream = st;
   cudaLaunchAttribute at[1];

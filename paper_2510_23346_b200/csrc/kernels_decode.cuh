@@ -120,7 +120,9 @@ struct DecSmem {
   static constexpr int kVsOff = kMiscOff + kMiscBytes;
   static constexpr int kVsBytes = kMt ? 0 : BN * kVsTok * 4;
   // B rows of the tile's columns: [32][128] bf16; LM 3: two 96-row chunk buffers (cp.async double buffering;
-  // both issued before the programmatic-dependency wait, so a share of <= 192 rows is in flight in one shot)
+  // both issued before the programmatic-dependency wait, so a share of <= 192 rows is in flight in one shot),
+  // stored as the MN-major no-swizzle operand of the tensor-core expand: (n, q) at
+  // (q/8)*2048 + (n/8)*128 + (q%8)*16 + (n%8)*2
   static constexpr int kBOff = kVsOff + kVsBytes;
   static constexpr int kMtRows = 96;
   static constexpr int kBBytes = kMt ? 2 * kMtRows * kDecBM * 2 : kDecLoraRows * kDecBM * 2;
@@ -128,11 +130,12 @@ struct DecSmem {
   static constexpr int kLrOff = kBOff + kBBytes;
   static constexpr int kLrBytes = 0;
   static constexpr int kLrCol = 2 * BN;
-  // LM 3: v of the tile's slice staged once, [T][C * Rc] fp32 (when it fits)
-  static constexpr int kVmOff = kLrOff + kLrBytes;
-  static constexpr int kVmFloats = kMt ? 8192 : 0;
+  // LM 3: the tensor-core expand's token operand of one chunk, V_hi | V_lo [64 tokens][kMtRows] bf16, K-major
+  // no-swizzle core-matrix layout (the B chunk above is the MN-major operand of the same MMA)
+  static constexpr int kVOpOff = kLrOff + kLrBytes;
+  static constexpr int kVOpHalf = kMt ? 64 * kMtRows * 2 : 0;
   // cluster split-K: [s][ceil(128/s)][16] fp32 partial slots the peers push into (<= (128 + s) x 16 floats)
-  static constexpr int kSlotOff = kVmOff + kVmFloats * 4;
+  static constexpr int kSlotOff = kVOpOff + 2 * kVOpHalf;
   static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * BN * 4 : 0;
   static constexpr int kBytes = kSlotOff + kSlotBytes + 1024;   // + 1024-B alignment slack
   static constexpr int kVCol = 2 * BN;                          // TMEM: [acc 0 | acc 1 | v_seg 0 | v_seg 1]
@@ -476,6 +479,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
+    if (L::kMt) ptx::mbar_init(reinterpret_cast<uint64_t*>(smem + L::kBarOff + 192), 1);
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
@@ -783,7 +787,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
           const int gq = dec_find_group(G.gq0, ng, q);
           src = p.arena + G.goffB[gq][jt] + (size_t)(q - G.gq0[gq]) * ldb + (nn - lo);
         }
-        ptx::cp_async_16_zfill(dst + rq * kDecBM + (e & 15) * 8, src, ok);
+        ptx::cp_async_16_zfill(dst + (rq >> 3) * 1024 + (e & 15) * 64 + (rq & 7) * 8, src, ok);
       }
       ptx::cp_async_commit();
       // the chunk's token list: (token, first expand row of its group inside the chunk, rows, chunk row offset)
@@ -807,8 +811,9 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
       }
     };
     bool mt_pre = false;
-    float* s_vm = reinterpret_cast<float*>(smem + L::kVmOff);
-    int vm_slice = -1;  // slice whose v s_vm holds
+    uint64_t* lbar = reinterpret_cast<uint64_t*>(smem + L::kBarOff + 192);  // LM 3: expand MMAs of a chunk done
+    uint32_t lphase = 0;
+    bool has_lr = false;
     if constexpr (L::kMt) {
       dec_groups64(G, p.ids, T, p.tab, etid, [] { ptx::named_bar_sync(1, 128); });
       if (etid == 0) DEC_TRACE(13);
@@ -962,81 +967,76 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
                                     : cta == dec_cta_of((long long)tile * p.k_blocks, UNITS, GRID)));
       if (LM == 2 && p.lora == 3 && ngroups > 0 && tile != cur_tile) stage_B(tile);
       if constexpr (L::kMt) {
-        // ---- LM 3: s_lr[t][row] = sum over this share's rows q of v[t][k(q)] B_{g(q)}[k(q)][n] (matmul_4 / _6
-        // of a precomputed v; only the rows of token t's own group contribute), B rows double-buffered
+        // ---- LM 3: LR[n][t] = sum over this share's rows q of B_{g(q)}[k(q)][n] V[t][q], V[t][q] = v[t][k(q)] when
+        // token t belongs to group g(q), else 0 (matmul_4 / _6 of a precomputed v) -- on the tensor cores, per
+        // 96-row chunk: A = the staged B rows (MN-major), B = V_hi + V_lo (bf16 split of fp32 v, K-major),
+        // accumulated in TMEM columns [kLrCol, kLrCol + 64) beside the base accumulator
         int tl, qlo, qhi;
         mt_range(u, tl, qlo, qhi);
-        // this tile's LoRA terms accumulate in TMEM columns [kLrCol, kLrCol + T) of this warp's lane quarter
-        const uint32_t lr_t = tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)L::kLrCol;
-        for (int c0 = 0; c0 < T; c0 += 16) ptx::tmem_st_zero_32x32b_x16(lr_t + c0);
-        ptx::tmem_st_wait();
         const int nchk = (qhi - qlo + L::kMtRows - 1) / L::kMtRows;
         if (!mt_pre) {
           if (nchk > 0) mt_stage(tile, qlo, qhi, 0);
           if (nchk > 1) mt_stage(tile, qlo + L::kMtRows, qhi, 1);
         }
         mt_pre = false;
-        const int jt = jlo, C = p.g.C, J = p.g.J, Rc = p.g.Rc, ng = G.ngroups;
-        const int vrow = C * Rc;  // s_vm row of a token: its C chunks of Rc
-        const bool use_vm = T * vrow <= L::kVmFloats;
-        if (use_vm && nchk > 0 && vm_slice != jt) {
-          // v of this slice for every token in one round of independent loads (v was written by the preceding
-          // kernel and is read many times per row below)
-          vm_slice = jt;
-          for (int i = etid; i < T * vrow; i += 128) {
-            const int t = i / vrow, r2 = i - t * vrow, c = r2 / Rc, kk = r2 - c * Rc;
-            s_vm[i] = __ldg(p.v + ((size_t)(c * T + t) * J + jt) * Rc + kk);
-          }
-        }
+        has_lr = nchk > 0;
+        const int jt = jlo, C = p.g.C, J = p.g.J, Rc = p.g.Rc;
+        const int4* lst = reinterpret_cast<const int4*>(reinterpret_cast<const uint8_t*>(mi) + L::kMtListOff);
+        const int* lcnt = mi + (L::kMtListOff + 2 * 2 * 32 * 16) / 4;
+        uint8_t* vop = smem + L::kVOpOff;
         if (u == u_lo && etid == 0) DEC_TRACE(14);
         for (int ch = 0; ch < nchk; ++ch) {
-          // chunks ch and ch + 1 are in flight (two groups): wait for the older one
-          if (ch + 1 < nchk) ptx::cp_async_wait_group<1>();
-          else ptx::cp_async_wait_group<0>();
+          if (ch > 0) {  // the previous chunk's MMAs have read V and their B buffer
+            ptx::mbar_wait(lbar, lphase);
+            lphase ^= 1u;
+            if (ch + 1 < nchk) mt_stage(tile, qlo + (ch + 1) * L::kMtRows, qhi, (ch + 1) & 1);
+          }
+          // V of this chunk: zero, then every listed token's rows (v fp32 -> bf16 hi + lo)
+          {
+            uint4* z = reinterpret_cast<uint4*>(vop);
+            for (int i = etid; i < 2 * L::kVOpHalf / 16; i += 128) z[i] = make_uint4(0u, 0u, 0u, 0u);
+          }
           ptx::named_bar_sync(1, 128);
-          const int qa = qlo + ch * L::kMtRows, qb = min(qhi, qa + L::kMtRows);
-          const uint16_t* sb = s_Bm + (ch & 1) * L::kMtRows * kDecBM + row;
-          const int4* lst = reinterpret_cast<const int4*>(reinterpret_cast<const uint8_t*>(mi) + L::kMtListOff);
-          const int* lcnt = mi + (L::kMtListOff + 2 * 2 * 32 * 16) / 4;
-#pragma unroll 1
-          for (int w = 0; w < 2; ++w) {
-            const int nl = lcnt[(ch & 1) * 2 + w];
-#pragma unroll 1
-            for (int e = 0; e < nl; ++e) {
-              const int4 en = lst[((ch & 1) * 2 + w) * 32 + e];
-              const int t = en.x, klo = en.y, nr = en.z;
-              const uint16_t* sbg = sb + en.w * kDecBM;
-              // the token's running LoRA term: loaded now, waited for after the dot (a token appears once per
-              // chunk, so no store of this chunk is pending on its column)
-              const uint32_t ta = lr_t + (uint32_t)t;
-              const uint32_t lr_old = ptx::tmem_ld_32x32b_x1(ta);
-              float s4[4] = {0.f, 0.f, 0.f, 0.f};
-              if (use_vm && C == 1) {
-                const float* vv = s_vm + t * vrow + klo;
-                int k = 0;
-                for (; k + 4 <= nr; k += 4) {
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) s4[q] = fmaf(vv[k + q], bf16_bits_to_f32(sbg[(k + q) * kDecBM]), s4[q]);
-                }
-                for (; k < nr; ++k) s4[k & 3] = fmaf(vv[k], bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
-              } else {
-                // generic: v from shared memory or global; S-LoRA column after the all-gather keeps rank row k
-                // in chunk k / (re / C)
-                const int rc = G.gre[G.grp[t]] / C;
-                for (int k = 0; k < nr; ++k) {
-                  const int kk = klo + k, c = kk / rc, kr = kk - c * rc;
-                  const float vk = use_vm ? s_vm[t * vrow + c * Rc + kr]
-                                          : __ldg(p.v + ((size_t)(c * T + t) * J + jt) * Rc + kr);
-                  s4[k & 3] = fmaf(vk, bf16_bits_to_f32(sbg[k * kDecBM]), s4[k & 3]);
-                }
-              }
-              ptx::tmem_ld_wait();  // warp-uniform list: whole-warp TMEM access
-              ptx::tmem_st_32x32b_x1(ta, __float_as_uint(__uint_as_float(lr_old) + ((s4[0] + s4[1]) + (s4[2] + s4[3]))));
+          const int b = ch & 1, n0l = lcnt[b * 2], nl = n0l + lcnt[b * 2 + 1];
+          for (int e = we; e < nl; e += 4) {  // a warp per listed token, lanes over its rows
+            const int4 en = e < n0l ? lst[(b * 2) * 32 + e] : lst[(b * 2 + 1) * 32 + (e - n0l)];
+            const int t = en.x, klo = en.y, nr = en.z, off = en.w;
+            const int rc = C > 1 ? G.gre[G.grp[t]] / C : 1;
+            for (int k = lane; k < nr; k += 32) {
+              const int kk = klo + k;
+              const int c = C > 1 ? kk / rc : 0, kr = C > 1 ? kk - c * rc : kk;
+              const float val = __ldg(p.v + ((size_t)(c * T + t) * J + jt) * Rc + kr);
+              const __nv_bfloat16 hi = __float2bfloat16_rn(val);
+              const __nv_bfloat16 lo = __float2bfloat16_rn(val - __bfloat162float(hi));
+              const int q = off + k;
+              const int o = (t >> 3) * (L::kMtRows / 8) * 128 + (q >> 3) * 128 + (t & 7) * 16 + (q & 7) * 2;
+              *reinterpret_cast<__nv_bfloat16*>(vop + o) = hi;
+              *reinterpret_cast<__nv_bfloat16*>(vop + L::kVOpHalf + o) = lo;
             }
           }
-          ptx::tmem_st_wait();  // this chunk's terms are in TMEM before the next chunk reloads a column
-          ptx::named_bar_sync(1, 128);  // chunk buffer (ch & 1) free for chunk ch + 2
-          if (ch + 2 < nchk) mt_stage(tile, qlo + (ch + 2) * L::kMtRows, qhi, ch & 1);
+          if (ch + 1 < nchk) ptx::cp_async_wait_group<1>();  // this chunk's B rows (the next one may be in flight)
+          else ptx::cp_async_wait_group<0>();
+          ptx::fence_proxy_async();  // generic-proxy shared-memory writes -> visible to the tensor core
+          ptx::named_bar_sync(1, 128);
+          if (etid == 0) {
+            ptx::tc_fence_after();
+            constexpr uint32_t idesc_mn = ptx::idesc_bf16_f32(kDecBM, BN) | (1u << 15);  // A operand MN-major
+            const uint32_t a0 = ptx::smem_u32(s_Bm + b * L::kMtRows * kDecBM), v0 = ptx::smem_u32(vop);
+            constexpr uint32_t kSboV = (L::kMtRows / 8) * 128;
+            const uint32_t d = tmem_base + (uint32_t)L::kLrCol;
+#pragma unroll
+            for (int kk = 0; kk < L::kMtRows / 16; ++kk) {
+              const uint64_t ad = ptx::sdesc_k_none(a0 + kk * 4096, /*LBO: q-group*/ 2048, /*SBO: n-group*/ 128);
+              ptx::mma_bf16(d, ad, ptx::sdesc_k_none(v0 + kk * 256, 128, kSboV), idesc_mn, (ch > 0 || kk > 0) ? 1u : 0u);
+              ptx::mma_bf16(d, ad, ptx::sdesc_k_none(v0 + L::kVOpHalf + kk * 256, 128, kSboV), idesc_mn, 1u);
+            }
+            ptx::mma_commit(lbar);
+          }
+        }
+        if (nchk > 0) {  // the tile's LoRA terms are in TMEM
+          ptx::mbar_wait(lbar, lphase);
+          lphase ^= 1u;
+          ptx::tc_fence_after();
         }
         if (u == u_lo && etid == 0) DEC_TRACE(15);
       }
@@ -1093,11 +1093,15 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
           if (BN == 16 && T == 1) {  // straight-line batch-1 path (no 16-way guarded unroll: i-cache)
             if (s_grp[0] == 0) lr[0] = dec_dot16(s_vs, bq);
           } else {
+            // branch-free: all 16 dots are independent (their shared loads and FMAs interleave); tokens past T or
+            // with id -1 are masked by a 0/1 factor (their v_seg rows are finite: zero-filled or real X rows)
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              lr[i] = (i < tn && s_grp[c0 + i] == 0) ? dec_dot16(s_vs + (c0 + i) * L::kVsTok, bq) : 0.f;
+            for (int i = 0; i < 16; ++i) {
+              const float w = (i < tn && s_grp[c0 + i] == 0) ? 1.f : 0.f;
+              lr[i] = w * dec_dot16(s_vs + (c0 + i) * L::kVsTok, bq);
+            }
           }
-        } else if (L::kMt) {
+        } else if (L::kMt && has_lr) {
           uint32_t l16[16];
           ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(L::kLrCol + c0), l16);
           ptx::tmem_ld_wait();
