@@ -161,7 +161,10 @@ int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* i
   cudaLaunchConfig_t cfg = {};
   // one item (A row) per CTA and pass, grid-stride: four CTAs per SM resident (<= 128 registers), so that
   // most batches take one pass; the GEMM's CTAs still fit beside them (no shared memory here but the tables)
-  static const int per_sm = std::max(1, env_int("BDLORA_SHRINK_CTAS_PER_SM", 4));
+  // measured (70B multi-tenant TP8, scripts/gpu_sweep_shrink.sh): 4 CTAs per SM for merged column projections
+  // (3 or 2 slices: the most A rows), 2 for single-slice ones (fewer items: less launch and residency cost)
+  static const int per_sm_env = env_int("BDLORA_SHRINK_CTAS_PER_SM", 0);
+  const int per_sm = per_sm_env > 0 ? per_sm_env : (g.J >= 2 ? 4 : 2);
   cfg.gridDim = dim3(std::max(1, per_sm * num_sms));
   cfg.blockDim = dim3(kDecShrinkThreads);
   cfg.stream = st;

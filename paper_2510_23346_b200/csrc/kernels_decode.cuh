@@ -358,13 +358,25 @@ __device__ __noinline__ void dec_vmode_lr(const DecParams* pp, int n, int t0, in
 
 // B rows of output column n = tile * 128 + row for every group of the batch: s_B[q][row] (bf16 bits), q = the
 // group's rank-row offset + k.  Out of line (called once per tile): keeps the kernel's executed code small.
+// canon (64-token tiles, one adapter, <= 16 rows): the 16 rows are written in the MN-major no-swizzle operand
+// layout of the tensor-core expand, (n, q) at element (q/8)*1024 + (n/8)*64 + (q%8)*8 + n%8, zeros past lrows.
 __device__ __noinline__ void dec_stage_B(const DecParams* pp, int tile, int row, int lrows, int ngroups,
-                                         const int* s_gq0, const long long* s_goff, uint16_t* s_B) {
+                                         const int* s_gq0, const long long* s_goff, uint16_t* s_B, int canon) {
   const DecParams& p = *pp;
   const int n = tile * kDecBM + row;
   const int jn = dec_slice_of(p.g, min(n, p.M - 1));
   const int lo = p.g.e_lo[jn], hi = p.g.e_hi[jn], ldb = hi - lo;
   const bool in = n < p.M && n >= lo && n < hi;
+  if (canon) {
+    uint16_t b[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      b[q] = (q < lrows && in) ? __ldg(reinterpret_cast<const uint16_t*>(p.arena + s_goff[3 + jn]) + (size_t)q * ldb + (n - lo))
+                               : (uint16_t)0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s_B[(q >> 3) * 1024 + (row >> 3) * 64 + (q & 7) * 8 + (row & 7)] = b[q];
+    return;
+  }
   for (int q0 = 0; q0 < lrows; q0 += 8) {  // 8 independent loads in flight, then 8 stores
     uint16_t b[8];
 #pragma unroll
@@ -479,7 +491,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 128);
     }
-    if (L::kMt) ptx::mbar_init(reinterpret_cast<uint64_t*>(smem + L::kBarOff + 192), 1);
+    if (L::kMt || (LM == 1 && BN == 64)) ptx::mbar_init(reinterpret_cast<uint64_t*>(smem + L::kBarOff + 192), 1);
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
@@ -729,7 +741,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
     const int lrows = lgrp ? mi[97] : 0;
     int cur_tile = -1;
     auto stage_B = [&](int tile) {
-      dec_stage_B(&p, tile, row, lrows, ngroups, s_gq0, s_goff, s_B);
+      dec_stage_B(&p, tile, row, lrows, ngroups, s_gq0, s_goff, s_B, (BN == 64 && LM == 1) ? 1 : 0);
       cur_tile = tile;
     };
     if (lgrp && ngroups > 0 && u_lo < u_hi) {
@@ -1050,7 +1062,48 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         // and this tile's B rows replace the previous tile's (each thread stages and reads only its own column)
         if (tile != cur_tile) stage_B(tile);
         ptx::named_bar_sync(1, 128);
-        if (q4 == 0) {
+        if constexpr (BN == 64) {
+          // 64-token tiles: the expand on the tensor cores, straight into the tile's accumulator --
+          // acc += B_rows^T (MN-major, staged canonically) x V^T, V[t][k] = s v_seg[k][t] split into bf16 hi + lo,
+          // zero for tokens with id -1 (their v_seg is real) and for rows k >= r/N
+          uint8_t* vop = reinterpret_cast<uint8_t*>(s_vs);
+          if (q4 == 0) {
+            const int rs = s_grs[0];
+            const float sc = s_gsc[0];
+#pragma unroll
+            for (int c0 = 0; c0 < BN; c0 += 16) {
+              uint32_t v16[16];
+              ptx::tmem_ld_32x32b_x16(tmem_base + (uint32_t)(L::kVCol + acc * BN + c0), v16);
+              ptx::tmem_ld_wait();
+              if (lane < 16) {
+#pragma unroll
+                for (int tt = 0; tt < 16; ++tt) {
+                  const int t = c0 + tt;
+                  const float val = (lane < rs && s_grp[t] == 0) ? sc * __uint_as_float(v16[tt]) : 0.f;
+                  const __nv_bfloat16 hi = __float2bfloat16_rn(val);
+                  const __nv_bfloat16 lo = __float2bfloat16_rn(val - __bfloat162float(hi));
+                  const int o = (t >> 3) * 256 + (lane >> 3) * 128 + (t & 7) * 16 + (lane & 7) * 2;
+                  *reinterpret_cast<__nv_bfloat16*>(vop + o) = hi;
+                  *reinterpret_cast<__nv_bfloat16*>(vop + 2048 + o) = lo;
+                }
+              }
+            }
+          }
+          ptx::fence_proxy_async();  // B rows and V (generic-proxy writes) -> visible to the tensor core
+          ptx::named_bar_sync(1, 128);
+          if (etid == 0) {
+            ptx::tc_fence_after();
+            constexpr uint32_t idesc_mn = ptx::idesc_bf16_f32(kDecBM, BN) | (1u << 15);  // A operand MN-major
+            const uint64_t ad = ptx::sdesc_k_none(ptx::smem_u32(s_B), /*LBO: q-group*/ 2048, /*SBO: n-group*/ 128);
+            const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+            ptx::mma_bf16(d, ad, ptx::sdesc_k_none(ptx::smem_u32(vop), 128, 256), idesc_mn, 1u);
+            ptx::mma_bf16(d, ad, ptx::sdesc_k_none(ptx::smem_u32(vop + 2048), 128, 256), idesc_mn, 1u);
+            ptx::mma_commit(lbar);
+          }
+          ptx::mbar_wait(lbar, lphase);
+          lphase ^= 1u;
+          ptx::tc_fence_after();
+        } else if (q4 == 0) {
           const int rs = s_grs[0];
           const float sc = s_gsc[0];
 #pragma unroll
@@ -1083,7 +1136,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         ptx::tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(acc * BN + c0), r);
         ptx::tmem_ld_wait();
         const int tn = min(16, T - c0);  // valid tokens of the chunk
-        if (tc) {
+        if (tc && BN == 16) {
           // this output column's B values of the adapter's rank rows in registers (zero past r/N), then one
           // 16-term dot per token against its v_seg row (broadcast 16-byte shared loads)
           float bq[16];

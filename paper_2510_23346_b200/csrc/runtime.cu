@@ -424,8 +424,9 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
     const bool staged = (int64_t)std::min<int64_t>(T, p->d.capacity) * p->re_max <= bdl::kDecLoraRowsHost;
     const bool mt = decode_mt_ok(p, T);
     int mode = 0;
-    if (staged && (T <= 16 || p->d.capacity == 1)) mode = 3;  // 17..64 tokens: one-adapter pools (BN = 64)
-    else if (mt) mode = 4;
+    if (staged && T <= 16) mode = 3;  // a few rank rows: staged once per tile, CUDA-core expand
+    else if (mt) mode = 4;            // tensor-core expand of the tile's rank rows (any number of adapters)
+    else if (staged && p->d.capacity == 1) mode = 3;
     else if (T <= 16) mode = 2;
     if (mode) {
       const int rc = launch_decode(p, X, T, W, ids, v, Y, ws, st, mode);

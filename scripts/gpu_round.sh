@@ -3,7 +3,7 @@
 # launch list of one eager layer step.  usage: scripts/gpu_round.sh TAG [what...]  what: test bench wl launches
 TAG=${1:-r2}
 shift
-WHAT=${@:-test bench wl launches}
+WHAT=${@:-test bench wl launches profile}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi_${TAG}.txt 2>&1
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_${TAG}.txt 2>&1
@@ -25,5 +25,18 @@ for w in $WHAT; do
       timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
         --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 2 --warmup 3 --no-graph --skip-slora \
         --skip-tp-emulation --skip-cpu --decode-layers 0 > /dev/null 2>&1 ;;
+    profile)
+      # ncu --set full of the dominant kernel (8B gate_up decode GEMM, T = 1) and of the 70B multi-tenant
+      # TP8 gate_up (lora 4); launch lists of the 8B prefill TP8 chain and of the multi-tenant TP8 QKV chain
+      timeout 300 ncu --set full --clock-control none --import-source on -k regex:dec_lora -s 3 -c 1 \
+        -o gpurun_out/prof_gateup_${TAG} -f python scripts/profile_one.py 28672 4096 1 16 fwd > /dev/null 2>&1
+      timeout 300 ncu --set full --clock-control none --import-source on -k regex:dec_lora -s 3 -c 1 \
+        -o gpurun_out/prof_mt_gateup_${TAG} -f python scripts/proj_profile.py llama-3.1-70b 2 8 64 8,16,32,64,128 128 uniform 4 > /dev/null 2>&1
+      timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed \
+        --clock-control none --csv --log-file gpurun_out/launches_prefill_${TAG}.csv \
+        python scripts/proj_profile.py llama-3.1-8b 2 8 1024 64 1 single 3 > /dev/null 2>&1
+      timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+        --log-file gpurun_out/launches_mt_${TAG}.csv python scripts/proj_profile.py llama-3.1-70b 0 8 64 8,16,32,64,128 128 uniform 3 > /dev/null 2>&1
+      for k in 0 1 2 3; do timeout 120 python scripts/proj_profile.py llama-3.1-8b $k 8 1024 64 1 single >> gpurun_out/prefill_${TAG}.txt 2>&1; done ;;
   esac
 done

@@ -26,7 +26,13 @@ VARIANTS = {
     "single_kernel_decode_forward": {"BDLORA_DECODE": "0"},  # the round-1 decode path instead of the lean kernel
 }
 
-# the lean decode kernel's own knobs (tests/test_gpu_decode.py)
+# the lean decode kernel's own knobs: a subset of tests/test_gpu_decode.py that covers every split / reduction
+# style (whole tiles, cluster DSMEM, global fix-up, stream-K), both token-tile widths and every LoRA mode
+DEC_SUBSET = ("(test_decode_8b_bs1_every_projection and (8-1 or 1-2 or 2-0)) or "
+              "(test_decode_integer_bit_exact and (5-8 or 16-2)) or "
+              "(test_decode_bn64_one_adapter and (0-8-64 or 2-8-64 or 0-1-64)) or "
+              "(test_decode_bn64_streamk_slices and True) or (test_decode_multi_adapter_vs_oracle and 17) or "
+              "test_decode_multi_adapter_integer_bit_exact or test_decode_v_precomputed_mode")
 DEC_VARIANTS = {
     "dec_streamk_all_sms": {"BDLORA_DEC_CTAS": "148"},
     "dec_two_stages": {"BDLORA_DEC_STAGES": "2"},
@@ -42,7 +48,7 @@ DEC_VARIANTS = {
 def test_decode_kernel_under_schedule_variant(name):
     env = dict(os.environ, **DEC_VARIANTS[name])
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_decode.py"), "-m", "gpu",
-                        "-x", "-q", "-p", "no:cacheprovider"],
+                        "-x", "-q", "-k", DEC_SUBSET, "-p", "no:cacheprovider"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     tail = "\n".join((r.stdout + r.stderr).strip().splitlines()[-15:])
     assert r.returncode == 0, f"{name} {DEC_VARIANTS[name]}:\n{tail}"
