@@ -156,7 +156,7 @@ int fit_cluster(int want, int need) {
 }  // namespace
 
 int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* ids, const SlotEntry* tab,
-                      const __nv_bfloat16* arena, float* v, int num_sms, cudaStream_t st, int pdl) {
+                      const __nv_bfloat16* arena, float* v, int num_sms, cudaStream_t st, int pdl, int rs_max) {
   if (T < 1 || T > kDecMaxT) return 1;
   cudaLaunchConfig_t cfg = {};
   // one item (A row) per CTA and pass, grid-stride: four CTAs per SM resident (<= 128 registers), so that
@@ -165,7 +165,9 @@ int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* i
   // (3 or 2 slices: the most A rows), 2 for single-slice ones (fewer items: less launch and residency cost)
   static const int per_sm_env = env_int("BDLORA_SHRINK_CTAS_PER_SM", 0);
   const int per_sm = per_sm_env > 0 ? per_sm_env : (g.J >= 2 ? 4 : 2);
-  cfg.gridDim = dim3(std::max(1, per_sm * num_sms));
+  // never more CTAs than the batch can have items (T x J x the pool's largest local shrink rank)
+  const long long items_max = (long long)T * g.J * std::max(1, rs_max);
+  cfg.gridDim = dim3((unsigned)std::max<long long>(1, std::min<long long>((long long)per_sm * num_sms, items_max)));
   cfg.blockDim = dim3(kDecShrinkThreads);
   cfg.stream = st;
   cudaLaunchAttribute at[1];

@@ -46,7 +46,7 @@ int dec_launch(const DecLaunch& a);
 // Multi-adapter shrink of a T <= 64 batch into v [T][J][Rc] fp32 (dec_shrink_kernel).  0 on launch, 1 if T is
 // out of range, negative on a CUDA error.
 int dec_shrink_launch(const Geom& g, const __nv_bfloat16* X, int T, const int* ids, const SlotEntry* tab,
-                      const __nv_bfloat16* arena, float* v, int num_sms, cudaStream_t st, int pdl);
+                      const __nv_bfloat16* arena, float* v, int num_sms, cudaStream_t st, int pdl, int rs_max);
 void dec_last_launch(int info[8]);
 void dec_set_trace(long long* buf);
 

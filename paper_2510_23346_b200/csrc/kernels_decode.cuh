@@ -1066,10 +1066,10 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
           // 64-token tiles: the expand on the tensor cores, straight into the tile's accumulator --
           // acc += B_rows^T (MN-major, staged canonically) x V^T, V[t][k] = s v_seg[k][t] split into bf16 hi + lo,
           // zero for tokens with id -1 (their v_seg is real) and for rows k >= r/N
+          // v_seg: TMEM lanes 0..15 (the lane-quarter-0 warp) -> fp32 staging, then all 128 threads build V
+          float* vst = reinterpret_cast<float*>(s_vs) + 1024;  // [16 k][64 t] fp32, behind the 4 KB of V
           uint8_t* vop = reinterpret_cast<uint8_t*>(s_vs);
           if (q4 == 0) {
-            const int rs = s_grs[0];
-            const float sc = s_gsc[0];
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 16) {
               uint32_t v16[16];
@@ -1077,16 +1077,26 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
               ptx::tmem_ld_wait();
               if (lane < 16) {
 #pragma unroll
-                for (int tt = 0; tt < 16; ++tt) {
-                  const int t = c0 + tt;
-                  const float val = (lane < rs && s_grp[t] == 0) ? sc * __uint_as_float(v16[tt]) : 0.f;
-                  const __nv_bfloat16 hi = __float2bfloat16_rn(val);
-                  const __nv_bfloat16 lo = __float2bfloat16_rn(val - __bfloat162float(hi));
-                  const int o = (t >> 3) * 256 + (lane >> 3) * 128 + (t & 7) * 16 + (lane & 7) * 2;
-                  *reinterpret_cast<__nv_bfloat16*>(vop + o) = hi;
-                  *reinterpret_cast<__nv_bfloat16*>(vop + 2048 + o) = lo;
-                }
+                for (int tt = 0; tt < 16; tt += 4)
+                  *reinterpret_cast<float4*>(vst + lane * 64 + c0 + tt) =
+                      make_float4(__uint_as_float(v16[tt]), __uint_as_float(v16[tt + 1]), __uint_as_float(v16[tt + 2]),
+                                  __uint_as_float(v16[tt + 3]));
               }
+            }
+          }
+          ptx::named_bar_sync(1, 128);
+          {
+            const int rs = s_grs[0];
+            const float sc = s_gsc[0];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {  // 1024 (token, row) values, 8 per thread
+              const int idx = etid + 128 * e, t = idx & 63, k = idx >> 6;
+              const float val = (k < rs && s_grp[t] == 0) ? sc * vst[k * 64 + t] : 0.f;
+              const __nv_bfloat16 hi = __float2bfloat16_rn(val);
+              const __nv_bfloat16 lo = __float2bfloat16_rn(val - __bfloat162float(hi));
+              const int o = (t >> 3) * 256 + (k >> 3) * 128 + (t & 7) * 16 + (k & 7) * 2;
+              *reinterpret_cast<__nv_bfloat16*>(vop + o) = hi;
+              *reinterpret_cast<__nv_bfloat16*>(vop + 2048 + o) = lo;
             }
           }
           ptx::fence_proxy_async();  // B rows and V (generic-proxy writes) -> visible to the tensor core

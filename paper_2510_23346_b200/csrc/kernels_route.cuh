@@ -61,10 +61,11 @@ __global__ void __launch_bounds__(1024) route_kernel(const int* __restrict__ ids
                                                      const SlotEntry* __restrict__ tab, Geom g, int* __restrict__ route,
                                                      float* __restrict__ v, int nv) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // ids may come from the preceding kernel
-  // the shrink GEMM accumulates v with fp32 reductions: start from zero
-  for (int i = threadIdx.x; i < nv; i += 1024) v[i] = 0.f;
+  // ids and the slot table are not written by the kernel preceding a forward (include/bdlora.h,
+  // bdlora_set_pdl), so segments and groups are found in shared memory while that kernel finishes; the
+  // workspace (route tables, v) is written only after the programmatic-dependency wait
   __shared__ int s_seg_id[kRouteMaxSeg];
+  __shared__ int s_grp_id[kRouteMaxGroups];  // the groups, kept here until the dependency wait
   __shared__ int s_warp[33];
   __shared__ int s_nseg, s_ngrp;
   const int tid = threadIdx.x;
@@ -102,22 +103,25 @@ __global__ void __launch_bounds__(1024) route_kernel(const int* __restrict__ ids
     }
     int tot;
     const int pos = s_ngrp + block_excl_scan_1024(lead, s_warp, &tot);
-    if (lead && pos < kRouteMaxGroups) route[RouteLayout::kGroupId + pos] = a;
+    if (lead && pos < kRouteMaxGroups) s_grp_id[pos] = a;
     __syncthreads();
     if (tid == 0) s_ngrp += tot;
     __syncthreads();
   }
   const int ngrp = min(s_ngrp, kRouteMaxGroups);
   if (s_ngrp > kRouteMaxGroups) overflow = 1;
-  __threadfence_block();
   __syncthreads();
+  // the route tables may still be read by a preceding kernel that shares this workspace (the previous
+  // forward's shrink): written only after the programmatic-dependency wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int gi = tid; gi < ngrp; gi += 1024) route[RouteLayout::kGroupId + gi] = s_grp_id[gi];
   // pass 4: items (16-row A boxes) per group, exclusive scan of the per-group counts
   int n_items = 0;
   for (int base = 0; base < ngrp; base += 1024) {
     const int gi = base + tid;
     int cnt = 0, a = -1, rs = 0;
     if (gi < ngrp) {
-      a = route[RouteLayout::kGroupId + gi];
+      a = s_grp_id[gi];
       rs = tab[a].rs;
       cnt = g.J * ((rs + 15) / 16);
     }
@@ -143,6 +147,8 @@ __global__ void __launch_bounds__(1024) route_kernel(const int* __restrict__ ids
     route[RouteLayout::kHdr + 1] = min(n_items, kRouteMaxItems);
     route[RouteLayout::kHdr + 2] = overflow;
   }
+  // the shrink GEMM accumulates v with fp32 reductions: start from zero
+  for (int i = threadIdx.x; i < nv; i += 1024) v[i] = 0.f;
 }
 
 }  // namespace bdl

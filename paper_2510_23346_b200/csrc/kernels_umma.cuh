@@ -1217,6 +1217,37 @@ inline int umma_bn_for_gemm(int M, int T, int num_sms) {
   return best;
 }
 
+// Compute-bound batches (T > 64) of the base GEMM: token-tile width AND cluster split-K together.  The kernel
+// is bound by each SM's operand ingress (~80 GB/s L2 -> shared memory), so the plan minimises the operand
+// bytes of the busiest CTA: (128 + BN) * K * 2 / s for a tile split s ways (s contributors of a cluster reduce
+// through DSMEM; their 128 x BN fp32 partials, pushed once, are counted at half weight), waves x (128 + BN) * K
+// * 2 for whole tiles beyond the SM count.  E.g. 8B QKV at TP8 (6 row tiles, T = 1024, K = 4096): BN 64 = 96
+// whole tiles (1.57 MB per CTA), BN 256 split 6 ways = 144 CTAs (0.52 MB + 128 KB of partials).
+inline void umma_tile_plan(int M, int K, int T, int num_sms, int* bn_out, int* split_out) {
+  const int bn0 = umma_bn_for(T);
+  const int m_tiles = (M + kUmmaBM - 1) / kUmmaBM, k_blocks = std::max(1, K / kUmmaBK);
+  double best = 1e300;
+  *bn_out = bn0;
+  *split_out = 1;
+  for (int bn = 64; bn <= bn0; bn *= 2) {
+    const long long tiles = (long long)m_tiles * ((T + bn - 1) / bn);
+    int s = 1;
+    double bytes;
+    if (tiles <= num_sms) {
+      s = (int)std::max<long long>(1, std::min<long long>(8, std::min<long long>(num_sms / tiles, k_blocks / 8)));
+      bytes = (128.0 + bn) * K * 2.0 / s + (s > 1 ? 0.5 * 128.0 * bn * 4.0 : 0.0);
+    } else {
+      const long long waves = (tiles + num_sms - 1) / num_sms;
+      bytes = (bn >= 128 ? (double)waves : (double)tiles / num_sms) * (128.0 + bn) * K * 2.0;
+    }
+    if (bytes < best * 0.95) {  // near-ties -> the wider tile (fewer X re-reads)
+      best = bytes;
+      *bn_out = bn;
+      *split_out = s;
+    }
+  }
+}
+
 // Counter region (fixed size, at a T-independent workspace offset, zero between launches):
 // [sync: 64 ints][split-tile counters: kUmmaMaxGrid ints]
 constexpr size_t kUmmaCounterBytes = 256 + kUmmaMaxGrid * sizeof(int);
@@ -1389,7 +1420,10 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
                        int tcx = 0, const CUtensorMap* amap = nullptr) {
   if (!umma_eligible(g, T)) return 1;
   if (v_fused && T > kFuseMaxT) return 1;
+  // (umma_tile_plan -- wider tiles split over a cluster -- measured slower: 8B QKV prefill at TP8 35.3 -> 42.0 us,
+  // TP4 40.2 -> 51.7 us; kept for reference, not used)
   const int BN = umma_bn_for_gemm(g.M, T, num_sms);
+  const int plan_split = 0;
   UmmaParams p;
   p.M = g.M;
   p.K = g.K;
@@ -1408,10 +1442,15 @@ inline int umma_launch(const Geom& g, const __nv_bfloat16* X, int T, const __nv_
   p.cluster = 1;
   if (tiles <= num_sms) {
     long long s = std::max<long long>(1, std::min<long long>(num_sms / tiles, p.k_blocks / 8));
-    if (BN >= 128) s = 1;  // compute-bound tiles: a split would move >= 64 KB of fp32 partials per contributor
+    long long sc = std::min<long long>(8, std::min<long long>(num_sms / tiles, p.k_blocks / 4));
+    if (plan_split > 0) {
+      // compute-bound tiles (T > 64): the tile plan's split, through a cluster (the partials are pushed once
+      // into the owners' idle weight rings); without clusters a compute-bound tile stays whole
+      s = cluster_splitk_enabled() ? plan_split : 1;
+      sc = s;
+    }
     // cluster split-K (the s contributors of a tile reduce through DSMEM): cheap fix-up, so split finer
-    const long long sc = std::min<long long>(8, std::min<long long>(num_sms / tiles, p.k_blocks / 4));
-    if (cluster_splitk_enabled() && BN <= 64 && sc >= 2) {
+    if (cluster_splitk_enabled() && sc >= 2) {
       s = sc;
       p.cluster = (int)sc;
     }

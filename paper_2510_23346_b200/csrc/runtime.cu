@@ -256,7 +256,7 @@ int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids
   if (T <= bdl::kDecMaxT && bdl::dec_enabled() && g.K % 8 == 0) {
     // decode-sized batch: one grid-wide launch, every distinct adapter's A rows read once
     const int rc = bdl::dec_shrink_launch(g, (const __nv_bfloat16*)X, T, ids, p->d_tab, (const __nv_bfloat16*)p->arena,
-                                          v, p->num_sms, st, g_pdl);
+                                          v, p->num_sms, st, g_pdl, p->rs_max);
     if (rc < 0) return fail(BDLORA_E_CUDA, "decode shrink launch: %s", cudaGetErrorString(cudaGetLastError()));
     if (rc == 0) {
       count_launch();
@@ -1053,7 +1053,7 @@ static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, con
     // decode batch over many adapters: grid-wide shrink (each distinct adapter's A rows read once), then the
     // decode kernel expands v in its epilogue (programmatic dependent launch: the weights stream meanwhile)
     const int rs = bdl::dec_shrink_launch(p->g, (const __nv_bfloat16*)X, (int)T, ids, p->d_tab,
-                                          (const __nv_bfloat16*)p->arena, v, p->num_sms, st, g_pdl);
+                                          (const __nv_bfloat16*)p->arena, v, p->num_sms, st, g_pdl, p->rs_max);
     if (rs < 0) return fail(BDLORA_E_CUDA, "decode shrink launch: %s", cudaGetErrorString(cudaGetLastError()));
     if (rs == 0) {
       count_launch();
