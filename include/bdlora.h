@@ -275,7 +275,9 @@ int bdlora_row_forward(bdlora_pool* pool, bdlora_comm* comm, const void* X, int6
    forward above on every device, then the base model's all-gather -- still no LoRA collective.
    Y [T, N * M_loc] bf16 = [Y_0 | Y_1 | ... | Y_{N-1}], the device blocks in rank order (for n_slices = 1
    exactly the full output X W + s X A B; for stacked slices the blocks keep their [q_i | k_i | v_i] order).
-   The workspace (bdlora_workspace_bytes) holds the [N][T][M_loc] staging of the in-place ncclAllGather.
+   T = 1: the device block is written straight into Y and gathered in place (the all-gather's rank-major
+   layout IS [Y_0 | ... | Y_{N-1}]).  T > 1: the workspace (bdlora_workspace_bytes) holds the
+   [N][T][M_loc] staging of the in-place ncclAllGather, interleaved into Y by one copy kernel.
    comm may be NULL iff tp_size == 1 (then it is bdlora_column_forward).  Pool: COLUMN + BD.          */
 int bdlora_column_forward_gather(bdlora_pool* pool, bdlora_comm* comm, const void* X, int64_t T, const void* W,
                                  const int32_t* ids, void* Y, void* workspace, size_t ws_bytes,

@@ -1130,9 +1130,17 @@ int bdlora_column_forward_gather(bdlora_pool* p, bdlora_comm* comm, const void* 
   cudaStream_t st = (cudaStream_t)stream;
   const int N = p->d.tp_size;
   if (N == 1) return bd_local(p, X, T, W, ids, Y, ws, st);
+  const size_t chunk = (size_t)T * p->g.M;
+  if (T == 1) {
+    // one token: [Y_0 | ... | Y_{N-1}] is the all-gather's own rank-major layout -- lines 3-6 straight into
+    // this rank's block of Y, then the all-gather in place (no staging buffer, no interleave pass)
+    __nv_bfloat16* Yb = (__nv_bfloat16*)Y;
+    ST_TRY(bd_local(p, X, T, W, ids, Yb + chunk * p->d.tp_rank, ws, st));
+    NC_TRY(ncclAllGather(Yb + chunk * p->d.tp_rank, Yb, chunk, ncclBfloat16, comm->nccl, st));
+    return BDLORA_OK;
+  }
   // Alg. 2 lines 3-6 into this rank's chunk of the staging buffer, then an in-place all-gather (line 8)
   __nv_bfloat16* G = (__nv_bfloat16*)((char*)ws + ws_layout(p, T).off_gather);
-  const size_t chunk = (size_t)T * p->g.M;
   ST_TRY(bd_local(p, X, T, W, ids, G + chunk * p->d.tp_rank, ws, st));
   // the base model's own collective: the LoRA counters of bdlora_comm_stats stay untouched
   NC_TRY(ncclAllGather(G + chunk * p->d.tp_rank, G, chunk, ncclBfloat16, comm->nccl, st));

@@ -22,7 +22,9 @@ dev = torch.device("cuda", 0)
 proj = synth.arch_projections(arch)[k]
 ranks = [ranks_l[a % len(ranks_l)] for a in range(n_ad)]
 par = bd.COLUMN if proj.parallel == "column" else bd.ROW
-pool = bd.bdlora_create_pool(par, bd.SHARD_BD, n, 0, proj.d_in, proj.d_out, n_ad, max(ranks))
+# SHARDING=slora: the S-LoRA device-local phases (shrink + v-precomputed expand, no collective)
+slora = os.environ.get("SHARDING", "bd") == "slora"
+pool = bd.bdlora_create_pool(par, bd.SHARD_SLORA if slora else bd.SHARD_BD, n, 0, proj.d_in, proj.d_out, n_ad, max(ranks))
 g = torch.Generator(device=dev)
 g.manual_seed(0)
 for a, r in enumerate(ranks):
@@ -30,9 +32,9 @@ for a, r in enumerate(ranks):
     for dj in proj.d_out:
         if proj.parallel == "column":
             A.append((torch.randn(proj.d_in, r, generator=g, device=dev) / 64).to(torch.bfloat16))
-            B.append((torch.randn(r // n, dj, generator=g, device=dev) / 8).to(torch.bfloat16))
+            B.append((torch.randn(r if slora else r // n, dj, generator=g, device=dev) / 8).to(torch.bfloat16))
         else:
-            A.append((torch.randn(proj.d_in, r // n, generator=g, device=dev) / 64).to(torch.bfloat16))
+            A.append((torch.randn(proj.d_in, r if slora else r // n, generator=g, device=dev) / 64).to(torch.bfloat16))
             B.append((torch.randn(r, dj, generator=g, device=dev) / 8).to(torch.bfloat16))
     bd.bdlora_load_adapter(pool, a, r, 1.0, A, B)
 nrep = max(2, math.ceil(3 * (126 << 20) / (pool.m_loc * pool.k_loc * 2)))
@@ -44,11 +46,16 @@ ids_np = {"single": lambda: np.zeros(T, np.int32), "uniform": lambda: synth.ids_
 ids = torch.from_numpy(ids_np).to(dev)
 Y = torch.empty(T, pool.m_loc, dtype=torch.bfloat16, device=dev)
 ws = bd.make_workspace(pool, T)
+if slora:
+    vbuf = torch.zeros((n if par == bd.COLUMN else 1) * bd.bdlora_v_elems(pool, T), dtype=torch.float32, device=dev)
 
 
 def fwd(i):
     W = Ws[i % nrep]
-    if par == bd.COLUMN:
+    if slora:
+        bd.bdlora_lora_shrink(pool, X, ids, vbuf, ws)
+        bd.bdlora_base_expand(pool, X, W, ids, vbuf, Y, ws)
+    elif par == bd.COLUMN:
         bd.bdlora_column_forward(pool, X, W, ids, Y, ws)
     else:
         bd.bdlora_row_partial(pool, X, W, ids, Y, ws)
