@@ -210,10 +210,15 @@ int bdlora_load_adapter(bdlora_pool* pool, int32_t slot, int32_t rank, float sca
    Device i runs the work of the N_h-layout devices i*m .. (i+1)*m - 1 (m = N_h/N_l) -- "stacking the
    computations of different devices": its A_1 / B_2 shards are the union of theirs (rank chunk
    [i r/N_l, (i+1) r/N_l)), and its local B_1 (COLUMN) or A_2 (ROW) is block-diagonal with those m
-   blocks, stored densely with explicit zeros (the same kernels run it; the zeros cost (m-1)/m of the
-   B_1 / A_2 shard bytes -- B_1, A_2 are r/N_l x d/N_l, small next to the base weight).  Load format =
-   bdlora_load_adapter's BD format with N_h in place of N.  BD pools only (E_MODE); N_l | N_h, N_h | r and
-   N_h | d_out[j] (COLUMN) or d_in (ROW) (E_DIVISIBILITY).  n_blocks == tp_size = bdlora_load_adapter. */
+   blocks.  Only the blocks are stored and read: COLUMN B_1 as [r/N_h, d_out_j/N_l] (the m
+   blocks side by side; the expand of block bb's columns reads v rows [bb r/N_h, (bb+1) r/N_h)), ROW A_2
+   as [r/N_l, d_in/N_h] (rank row q holds the inputs of its block q / (r/N_h) only).  A pool holds one
+   block count m: loading an adapter with another m while others are resident is E_MODE.  Pools with
+   m > 1 run every batch through the multi-adapter decode kernels, in chunks of <= 64 tokens (the base
+   weights are streamed once per chunk).  Load format = bdlora_load_adapter's BD format with N_h in place
+   of N.  BD pools only (E_MODE); N_l | N_h, N_h | r and N_h | d_out[j] (COLUMN) or d_in (ROW); m > 1 also
+   needs 128-column-aligned slices with blocks of a multiple of 8 columns (COLUMN) or 8 | d_in/N_h and
+   64 | d_in/N_l (ROW) (E_DIVISIBILITY).  n_blocks == tp_size = bdlora_load_adapter.                  */
 int bdlora_load_adapter_blocks(bdlora_pool* pool, int32_t slot, int32_t rank, float scale,
                                const void* const* A, const void* const* B, int32_t n_blocks,
                                int32_t src_is_device, bdlora_stream_t stream);

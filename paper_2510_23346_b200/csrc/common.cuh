@@ -36,6 +36,12 @@ struct Geom {
   int e_hi[kMaxSlices];
   int Rc;                 // per-chunk rank capacity of v
   int C;                  // chunks of v read by the expand (S-LoRA column after all-gather: N)
+  // downward-compatible serving: m = N_h / N local diagonal blocks per resident adapter, stored
+  // compactly -- no zero is stored or read.  bblk = m for COLUMN pools (B_1 local = m blocks [r/N_h, w/m] side
+  // by side: [r/N_h, w]), ablk = m for ROW pools (A_2 local = m blocks [d_in/N_h, r/N_h]: rank row q of block
+  // q / (r/N_h) holds only its block's K/m inputs).  1 = native BD (one block per device).
+  int ablk;
+  int bblk;
 };
 
 // Profiling stamp inside lora_chunk16 (bdlora_debug_trace): %globaltimer into slot k of this CTA's trace row

@@ -114,7 +114,9 @@ struct DecSmem {
   // ... [960, 1024) group of each of up to 64 tokens.  LM 3: a DecGroups.
   static constexpr int kMiscBytes = kMt ? 12288 : 4096;
   static constexpr int kMtListOff = 8192;  // LM 3: per chunk buffer and warp, the tokens whose group meets the chunk
+  static constexpr int kMtRowOff = 10496;  // LM 3: arena offset of each staged chunk row (96 x 8 B)
   static_assert(!kMt || sizeof(DecGroups) <= kMtListOff, "group tables");
+  static_assert(kMtRowOff >= kMtListOff + 2 * 2 * 32 * 16 + 16 && kMtRowOff + 96 * 12 <= 12288 - 16, "row table");
   // v_seg: BN = 16: [16 tokens][3 slices][32] fp32; BN = 64 (one adapter, one slice per tile): [64][32]
   static constexpr int kVsTok = BN == 16 ? 3 * kDecLoraRows : kDecLoraRows;
   static constexpr int kVsOff = kMiscOff + kMiscBytes;
@@ -240,8 +242,8 @@ __device__ __forceinline__ int dec_find_group(const int* pre, int ng, int q) {
 
 // Multi-adapter LoRA shrink of a decode batch (matmul_3 / matmul_5 for T <= 64 tokens over many adapters,
 // P:287-288):  v[t][j][k] = s_a(t) X[t] . A_{a(t),j}[k]  (fp32, scaled; layout [T][J][Rc]).
-// Work item = one (token, slice, rank row) dot product of length K: four warps share an item (one K quarter
-// each, 8 A + 8 X 16-byte loads in flight per lane), fixed-order reduction (deterministic).  Tokens of one
+// Work item = one (token, slice, rank row) dot product of length K: 1, 2 or 4 warps share an item (K <= 2048,
+// <= 4096, longer: <= 8 A + 8 X 16-byte loads in flight per lane), fixed-order reduction (deterministic).  Tokens of one
 // adapter read the same A rows (L2 hits after the first).  Launched before the decode GEMM with programmatic
 // dependent launch: the GEMM streams its weights (and stages its B rows) while this runs.
 constexpr int kDecShrinkThreads = 128;
@@ -288,9 +290,16 @@ __global__ void __launch_bounds__(kDecShrinkThreads, 4) dec_shrink_kernel(const 
   if (tid == 0 && !late_trigger) ptx::pdl_launch_dependents();
   if (pdl) ptx::pdl_wait();                    // X is written by the preceding kernel
   const int items = s_pre[64];
-  const int nch = K >> 3;  // 16-byte chunks of a row
-  const int c_lo = (nch * warp) >> 2, c_hi = (nch * (warp + 1)) >> 2;
-  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+  // downward-compatible ROW pool (g.ablk = m > 1): rank row k of block b = k / (rs/m) is stored compactly with
+  // its block's K/m inputs only and dots X[t][b K/m, (b+1) K/m) -- no zero of the block-diagonal A_2 is read
+  const int ab = g.ablk > 1 ? g.ablk : 1, kl = K / ab;
+  const int nch = kl >> 3;  // 16-byte chunks of a row
+  // wpi warps per item (a lane keeps <= 8 chunks of A and X in flight per pass): short rows take one warp each,
+  // so a CTA works on 4 / wpi items at once (the latency of one L2 round trip per item, not per CTA)
+  const int wpi = kl <= 2048 ? 1 : (kl <= 4096 ? 2 : 4);
+  const int gpc = 4 / wpi, grp = warp / wpi, sub = warp - grp * wpi;
+  const int c_lo = (nch * sub) / wpi, c_hi = (nch * (sub + 1)) / wpi;
+  for (int it = blockIdx.x * gpc + grp; it < items; it += gridDim.x * gpc) {
     int lo = 0, hi = 63;  // token: largest t with s_pre[t] <= it
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -299,8 +308,8 @@ __global__ void __launch_bounds__(kDecShrinkThreads, 4) dec_shrink_kernel(const 
     }
     const int t = lo, rs = s_rs[t];
     const int r = it - s_pre[t], j = r / rs, k = r - j * rs;
-    const __nv_bfloat16* Arow = arena + s_offA[t][j] + (size_t)k * K;
-    const __nv_bfloat16* Xrow = X + (size_t)t * K;
+    const __nv_bfloat16* Arow = arena + s_offA[t][j] + (size_t)k * kl;
+    const __nv_bfloat16* Xrow = X + (size_t)t * K + (size_t)(ab > 1 ? k / (rs / ab) : 0) * kl;
     float acc = 0.f, acc2 = 0.f;
 #pragma unroll 1
     for (int cb = c_lo; cb < c_hi; cb += 256) {  // 8 chunks per lane per block (one block at K = 8192)
@@ -324,10 +333,17 @@ __global__ void __launch_bounds__(kDecShrinkThreads, 4) dec_shrink_kernel(const 
       }
     }
     const float ws = warp_sum(acc + acc2);
-    if (lane == 0) s_red[warp] = ws;
-    __syncthreads();
-    if (tid == 0) v[((size_t)t * J + j) * g.Rc + k] = s_sc[t] * ((s_red[0] + s_red[1]) + (s_red[2] + s_red[3]));
-    __syncthreads();
+    float* vo = v + ((size_t)t * J + j) * g.Rc + k;
+    if (wpi == 1) {
+      if (lane == 0) *vo = s_sc[t] * ws;
+    } else {  // fixed-order sum of the item's warps (deterministic)
+      if (lane == 0) s_red[warp] = ws;
+      ptx::named_bar_sync(1 + grp, wpi * 32);
+      if (sub == 0 && lane == 0)
+        *vo = s_sc[t] * (wpi == 2 ? s_red[warp] + s_red[warp + 1]
+                                  : (s_red[warp] + s_red[warp + 1]) + (s_red[warp + 2] + s_red[warp + 3]));
+      ptx::named_bar_sync(1 + grp, wpi * 32);
+    }
   }
   if (tid == 0 && late_trigger) ptx::pdl_launch_dependents();
 }
@@ -767,6 +783,16 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
     uint16_t* s_Bm = reinterpret_cast<uint16_t*>(smem + L::kBOff);
     // this contributor's share [qlo, qhi) of the tile's expand rows (every contributor of a split tile takes
     // a contiguous share: the LoRA term is linear and rides the split-K reduction)
+    // downward-compatible COLUMN pool (g.bblk = m > 1, B_1 local = m diagonal blocks stored compactly as
+    // [r/N_h, w]): a tile meets the diagonal blocks bb0 .. bb0 + nblk - 1 of its slice, and every group
+    // contributes nblk x (its r/N_h) expand rows to it (v rows [bb0 r/N_h, (bb0 + nblk) r/N_h)); m = 1: one block
+    const int bbk = p.g.bblk > 1 ? p.g.bblk : 1;
+    auto tile_blocks = [&](int n0, int jt, int& bb0, int& nblk, int& blkw) {
+      const int c0 = p.g.col0[jt], w = p.g.col0[jt + 1] - c0;
+      blkw = w / bbk;
+      bb0 = (n0 - c0) / blkw;
+      nblk = (min(n0 + kDecBM, c0 + w) - 1 - c0) / blkw - bb0 + 1;
+    };
     auto mt_range = [&](int u, int& tile, int& qlo, int& qhi) {
       tile = u / p.k_blocks;
       const int kb0 = u - tile * p.k_blocks, kb1 = min(p.k_blocks, kb0 + (u_hi - u));
@@ -780,37 +806,72 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         ci = cta - c_first;
         ns = c_last - c_first + 1;
       }
-      qlo = (int)((long long)G.qtot * ci / ns);
-      qhi = (int)((long long)G.qtot * (ci + 1) / ns);
       const int n0 = tile * kDecBM, jt = dec_slice_of(p.g, n0);
+      int bb0, nblk, blkw;
+      tile_blocks(n0, jt, bb0, nblk, blkw);
+      const int qt = G.qtot / bbk * nblk;  // this tile's expand rows
+      qlo = (int)((long long)qt * ci / ns);
+      qhi = (int)((long long)qt * (ci + 1) / ns);
       if (n0 >= p.g.e_hi[jt] || n0 + kDecBM <= p.g.e_lo[jt]) qhi = qlo;  // tile outside the expand window
     };
     // rows [qa, qa + 64) of the share, this tile's 128 columns, into chunk buffer `buf` (zeros past the window)
+    int mt_calls = 0;  // profiling stamps of the third call (chunk 2's rows)
     auto mt_stage = [&](int tile, int qa, int qhi, int buf) {
       const int n0 = tile * kDecBM, jt = dec_slice_of(p.g, n0);
       const int lo = p.g.e_lo[jt], hi = p.g.e_hi[jt], ldb = hi - lo;
       uint16_t* dst = s_Bm + buf * L::kMtRows * kDecBM;
       const int qb = min(qhi, qa + L::kMtRows), ng = G.ngroups;
-      for (int e = etid; e < L::kMtRows * 16; e += 128) {
-        const int rq = e >> 4, nn = n0 + (e & 15) * 8, q = qa + rq;
-        const bool ok = q < qb && nn >= lo && nn < hi;
-        const __nv_bfloat16* src = p.arena;
-        if (ok) {
+      // the arena offset of each row's window start, once per row (one thread each), then 16 B per thread
+      long long* rowoff = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(mi) + L::kMtRowOff);
+      int* rowblk = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(mi) + L::kMtRowOff + L::kMtRows * 8);
+      int bb0, nblk, blkw;
+      tile_blocks(n0, jt, bb0, nblk, blkw);
+      if (etid < L::kMtRows) {
+        const int q = qa + etid;
+        long long o = -1;
+        int blk = -1;
+        if (q < qb && bbk == 1) {
           const int gq = dec_find_group(G.gq0, ng, q);
-          src = p.arena + G.goffB[gq][jt] + (size_t)(q - G.gq0[gq]) * ldb + (nn - lo);
+          o = G.goffB[gq][jt] + (long long)(q - G.gq0[gq]) * ldb - lo;
+          blk = 0;
+        } else if (q < qb) {
+          // group: the last g whose first row in this tile's numbering, gq0[g] / m * nblk, is <= q
+          int g0 = 0, g1 = ng - 1;
+          while (g0 < g1) {
+            const int mid = (g0 + g1 + 1) >> 1;
+            if (G.gq0[mid] / bbk * nblk <= q) g0 = mid;
+            else g1 = mid - 1;
+          }
+          const int qq = q - G.gq0[g0] / bbk * nblk, rbg = G.gre[g0] / bbk, bi = qq / rbg;
+          blk = bb0 + bi;
+          o = G.goffB[g0][jt] + (long long)(qq - bi * rbg) * ldb - lo;  // row qq - bi rbg of the compact B
         }
-        ptx::cp_async_16_zfill(dst + (rq >> 3) * 1024 + (e & 15) * 64 + (rq & 7) * 8, src, ok);
+        rowoff[etid] = o;
+        rowblk[etid] = blk;
+      }
+      ptx::named_bar_sync(1, 128);
+      if (etid == 0 && mt_calls == 2) DEC_TRACE(10);
+      const int c0s = p.g.col0[jt];
+      for (int e = etid; e < L::kMtRows * 16; e += 128) {
+        const int rq = e >> 4, nn = n0 + (e & 15) * 8;
+        const long long o = rowoff[rq];
+        // 8 columns of one row: inside the window and (m > 1) inside the row's own diagonal block
+        const bool ok = o >= 0 && nn >= lo && nn < hi && (bbk == 1 || (nn - c0s) / blkw == rowblk[rq]);
+        ptx::cp_async_16_zfill(dst + (rq >> 3) * 1024 + (e & 15) * 64 + (rq & 7) * 8, ok ? p.arena + o + nn : p.arena, ok);
       }
       ptx::cp_async_commit();
+      if (etid == 0 && mt_calls++ == 2) DEC_TRACE(30);
       // the chunk's token list: (token, first expand row of its group inside the chunk, rows, chunk row offset)
       // for every token whose group's rows meet [qa, qb) -- built by the first two epilogue warps
       if (etid < 64) {
         int klo = 0, nr = 0, off = 0;
         const int gt = etid < T ? G.grp[etid] : -1;
         if (gt >= 0) {
-          const int q0 = G.gq0[gt], qlo2 = max(qa, q0), qhi2 = min(qb, q0 + G.gre[gt]);
+          // the group's rows in this tile: [q0, q0 + nblk r/N_h), v rows from bb0 r/N_h on (m = 1: [0, r/N))
+          const int q0 = bbk == 1 ? G.gq0[gt] : G.gq0[gt] / bbk * nblk, rbg = bbk == 1 ? G.gre[gt] : G.gre[gt] / bbk;
+          const int qlo2 = max(qa, q0), qhi2 = min(qb, q0 + nblk * rbg);
           if (qlo2 < qhi2) {
-            klo = qlo2 - q0;
+            klo = bb0 * rbg + (qlo2 - q0);
             nr = qhi2 - qlo2;
             off = qlo2 - qa;
           }
@@ -834,7 +895,10 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         mt_range(u_lo, tile, qlo, qhi);
         if (qlo < qhi) {
           mt_stage(tile, qlo, qhi, 0);
-          if (qhi - qlo > L::kMtRows) mt_stage(tile, qlo + L::kMtRows, qhi, 1);
+          if (qhi - qlo > L::kMtRows) {
+            ptx::named_bar_sync(1, 128);  // every thread is past the first call's row-table reads
+            mt_stage(tile, qlo + L::kMtRows, qhi, 1);
+          }
           mt_pre = true;
         }
       }
@@ -988,7 +1052,10 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         const int nchk = (qhi - qlo + L::kMtRows - 1) / L::kMtRows;
         if (!mt_pre) {
           if (nchk > 0) mt_stage(tile, qlo, qhi, 0);
-          if (nchk > 1) mt_stage(tile, qlo + L::kMtRows, qhi, 1);
+          if (nchk > 1) {
+            ptx::named_bar_sync(1, 128);  // every thread is past the first call's row-table reads
+            mt_stage(tile, qlo + L::kMtRows, qhi, 1);
+          }
         }
         mt_pre = false;
         has_lr = nchk > 0;
@@ -1001,8 +1068,10 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
           if (ch > 0) {  // the previous chunk's MMAs have read V and their B buffer
             ptx::mbar_wait(lbar, lphase);
             lphase ^= 1u;
+            if (u == u_lo && etid == 0 && ch == 1) DEC_TRACE(5);
             if (ch + 1 < nchk) mt_stage(tile, qlo + (ch + 1) * L::kMtRows, qhi, (ch + 1) & 1);
           }
+          if (u == u_lo && etid == 0 && ch < 7) DEC_TRACE(16 + 2 * ch);
           // V of this chunk: zero, then every listed token's rows (v fp32 -> bf16 hi + lo)
           {
             uint4* z = reinterpret_cast<uint4*>(vop);
@@ -1030,6 +1099,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
           else ptx::cp_async_wait_group<0>();
           ptx::fence_proxy_async();  // generic-proxy shared-memory writes -> visible to the tensor core
           ptx::named_bar_sync(1, 128);
+          if (u == u_lo && etid == 0 && ch < 7) DEC_TRACE(17 + 2 * ch);
           if (etid == 0) {
             ptx::tc_fence_after();
             constexpr uint32_t idesc_mn = ptx::idesc_bf16_f32(kDecBM, BN) | (1u << 15);  // A operand MN-major

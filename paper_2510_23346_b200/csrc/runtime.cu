@@ -137,11 +137,15 @@ void ranks_for(const bdlora_pool* p, int r, int* rs, int* re) {
   }
 }
 
-int64_t slot_elems_for_rank(const bdlora_pool* p, int r) {
+// m > 1: a downward-compatible adapter's compact local blocks -- COLUMN: B_j [r/N_h, w] (the m
+// diagonal blocks side by side), ROW: A [r/N, K/m] (rank row q holds only its block's inputs)
+int64_t slot_elems_for_rank(const bdlora_pool* p, int r, int m = 1) {
   int rs, re;
   ranks_for(p, r, &rs, &re);
+  const bool row = p->d.parallel == BDLORA_ROW;
   int64_t e = 0;
-  for (int j = 0; j < p->g.J; ++j) e += (int64_t)rs * p->g.K + (int64_t)re * p->ldb[j];
+  for (int j = 0; j < p->g.J; ++j)
+    e += (int64_t)rs * p->g.K / (row ? m : 1) + (int64_t)(row ? re : re / m) * p->ldb[j];
   // slot regions are whole rows of K elements: every A row starts at a multiple of K, so one TMA
   // tensor map over the arena ([arena_elems / K, K]) addresses any adapter's A rows (tensor-core shrink)
   const int64_t K = p->g.K;
@@ -241,6 +245,11 @@ int check_fwd_args(const bdlora_pool* p, const void* X, int64_t T, const void* W
 
 // ---------------------------------------------------------------------------- launches
 int g_pdl = 1;  // programmatic dependent launch chaining (bdlora_set_pdl)
+
+// Downward-compatible pools (compact local blocks, Geom::ablk / bblk > 1) run every batch through the
+// multi-adapter decode path -- dec_shrink_kernel (block-local K window for ROW pools) then the decode kernel's
+// tensor-core expand (block-local rank rows for COLUMN pools) -- in chunks of <= 64 tokens.
+bool pool_blocked(const bdlora_pool* p) { return p->g.ablk > 1 || p->g.bblk > 1; }
 thread_local bdlora_peer* g_push = nullptr;  // set around the decode launch of bdlora_row_partial_push
 
 WsLayout ws_layout(const bdlora_pool* p, int64_t T);
@@ -253,6 +262,18 @@ int launch_shrink(const bdlora_pool* p, const void* X, int T, const int32_t* ids
                   void* ws = nullptr) {
   if (T == 0) return BDLORA_OK;
   const Geom& g = p->g;
+  if (pool_blocked(p)) {
+    for (int c0 = 0; c0 < T; c0 += bdl::kDecMaxT) {
+      const int Tc = std::min(T - c0, bdl::kDecMaxT);
+      const int rc = bdl::dec_shrink_launch(g, (const __nv_bfloat16*)X + (size_t)c0 * g.K, Tc, ids + c0, p->d_tab,
+                                            (const __nv_bfloat16*)p->arena, v + (size_t)c0 * g.J * g.Rc, p->num_sms,
+                                            st, g_pdl, p->rs_max);
+      if (rc != 0) return fail(BDLORA_E_CUDA, "decode shrink launch (%d): %s", rc, cudaGetErrorString(cudaGetLastError()));
+      count_launch();
+      g_last_src = 1;
+    }
+    return BDLORA_OK;
+  }
   if (T <= bdl::kDecMaxT && bdl::dec_enabled() && g.K % 8 == 0) {
     // decode-sized batch: one grid-wide launch, every distinct adapter's A rows read once
     const int rc = bdl::dec_shrink_launch(g, (const __nv_bfloat16*)X, T, ids, p->d_tab, (const __nv_bfloat16*)p->arena,
@@ -393,7 +414,7 @@ int launch_decode(const bdlora_pool* p, const void* X, int T, const void* W, con
 // K-local LoRA inside the decode kernel needs every adapter's shrink and expand device-local (BD / NFS, one v
 // chunk) and the batch's distinct adapters to fit the kernel's rank-row capacity in the worst case.
 bool decode_klocal_ok(const bdlora_pool* p, int T) {
-  if (p->d.sharding == BDLORA_SHARD_SLORA || p->g.C != 1) return false;
+  if (p->d.sharding == BDLORA_SHARD_SLORA || p->g.C != 1 || pool_blocked(p)) return false;
   if (T > 16) {
     // 17..64 tokens (BN = 64 tiles): only the tensor-core K-local shrink is compiled there -- one adapter per
     // pool, r/N <= 16, every tile inside one slice, the arena's A-row map
@@ -418,6 +439,18 @@ int launch_base_expand(const bdlora_pool* p, const void* X, int T, const void* W
                        void* Y, void* ws, cudaStream_t st) {
   const int pdl = g_pdl;
   if (T == 0) return BDLORA_OK;
+  if (pool_blocked(p)) {
+    if (!decode_mt_ok(p, 1))
+      return fail(BDLORA_E_ARG, "downward-compatible pool: the multi-adapter decode kernel cannot serve this "
+                  "geometry (K %% 64, 128-column slices) or it is disabled (BDLORA_DECODE=0)");
+    for (int c0 = 0; c0 < T; c0 += bdl::kDecMaxT) {
+      const int Tc = std::min(T - c0, bdl::kDecMaxT);
+      const int rc = launch_decode(p, (const __nv_bfloat16*)X + (size_t)c0 * p->g.K, Tc, W, ids + c0,
+                                   v + (size_t)c0 * p->g.J * p->g.Rc, (__nv_bfloat16*)Y + (size_t)c0 * p->g.M, ws, st, 4);
+      if (rc != BDLORA_OK) return rc < 0 ? fail(BDLORA_E_ARG, "downward-compatible expand: shape not served") : rc;
+    }
+    return BDLORA_OK;
+  }
   if (bdl::dec_enabled() && bdl::dec_eligible(p->g, T)) {
     // v precomputed: staged-B expand (mode 3) when the batch's distinct adapters fit the kernel's rank-row
     // capacity in the worst case, else the per-output gather (mode 2)
@@ -600,6 +633,7 @@ int bdlora_create_pool(const bdlora_pool_desc* desc, int cuda_device, bdlora_poo
   p->dev = cuda_device;
   Geom& g = p->g;
   memset(&g, 0, sizeof(g));
+  g.ablk = g.bblk = 1;  // native BD until a downward-compatible adapter is loaded (bdlora_load_adapter_blocks)
   const int i = d.tp_rank;
   if (d.parallel == BDLORA_COLUMN) {
     g.K = d.d_in;
@@ -791,7 +825,28 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
 
   int rs, re;
   ranks_for(p, rank, &rs, &re);
-  const int64_t elems = slot_elems_for_rank(p, rank);
+  // downward-compatible serving: m = N_h / N blocks per device, one m per pool (the kernels read it from the
+  // geometry); the compact blocks are all that is stored
+  const int m = (d.sharding == BDLORA_SHARD_BD && nb > 0) ? nb / N : 1;
+  const bool row = d.parallel == BDLORA_ROW;
+  {
+    int others = 0;
+    for (int s2 = 0; s2 < d.capacity; ++s2) others += (s2 != slot && p->h_tab[s2].loaded) ? 1 : 0;
+    const int cur_m = row ? p->g.ablk : p->g.bblk;
+    if (others > 0 && cur_m != m)
+      return fail(BDLORA_E_MODE, "pool holds adapters with %d local block(s) per device; this load has %d (one "
+                  "block count per pool)", cur_m, m);
+    if (m > 1) {
+      if (row && ((p->g.K / m) % 8 || p->g.K % 64))
+        return fail(BDLORA_E_DIVISIBILITY, "downward-compatible ROW pool: K/m = %d must be a multiple of 8 and "
+                    "K = %d of 64", p->g.K / m, p->g.K);
+      for (int j = 0; j < J && !row; ++j)
+        if (p->g.col0[j] % 128 || (p->ldb[j] / m) % 8)
+          return fail(BDLORA_E_DIVISIBILITY, "downward-compatible COLUMN pool: slice %d must start on a 128-column "
+                      "boundary (%d) with blocks of a multiple of 8 columns (%d)", j, p->g.col0[j], p->ldb[j] / m);
+    }
+  }
+  const int64_t elems = slot_elems_for_rank(p, rank, m);
   int64_t off = 0;
   ST_TRY(arena_alloc(p, slot, elems, &off));
   auto retire_old = [&]() {
@@ -828,7 +883,7 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
   };
   int rc = BDLORA_OK;
   // slot layout [A_0 | A_1 | A_2 | B_0 | B_1 | B_2]: every A block starts on a K-row boundary
-  int64_t curB = cur + (int64_t)J * rs * K;
+  int64_t curB = cur + (int64_t)J * rs * K / (row ? m : 1);
   for (int j = 0; j < J && rc == BDLORA_OK; ++j) {
     const int dout = d.d_out[j];
     const int w = p->ldb[j];
@@ -857,15 +912,15 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
       cur += (int64_t)rs * K;
     } else if (d.sharding == BDLORA_SHARD_BD) {
       // downward-compatible: compact d_in x r/N_h with N_h stacked blocks; this device runs the
-      // blocks b = i*m + bb (m = N_h/N): the local A_2 is block-diagonal, stored transposed [r/N, d_in/N]
-      const int m = nb / N, rb = rank / nb, kb = d.d_in / nb;
+      // blocks b = i*m + bb (m = N_h/N).  Stored compactly, transposed: rank row q = bb * r/N_h + k holds the
+      // K/m inputs of its block only, [r/N, K/m] -- the zeros of the block-diagonal A_2 are never stored
+      const int rb = rank / nb, kb = d.d_in / nb;
       rc = src_ptr(A[0], (int64_t)d.d_in * rb, &sa);
       if (rc) break;
       e.offA[0] = cur;
-      if (cudaMemsetAsync(p->arena + cur, 0, (size_t)rs * K * 2, st) != cudaSuccess) rc = fail(BDLORA_E_CUDA, "memset");
       for (int bb = 0; bb < m && rc == BDLORA_OK; ++bb)
-        rc = gather_to(sa, rb, (i * m + bb) * kb, 0, kb, rb, 1, p->arena + cur + (int64_t)bb * rb * K + bb * kb, st, K);
-      cur += (int64_t)rs * K;
+        rc = gather_to(sa, rb, (i * m + bb) * kb, 0, kb, rb, 1, p->arena + cur + (int64_t)bb * rb * kb, st, kb);
+      cur += (int64_t)rs * kb;
     } else {
       // S-LoRA / NFS row: A_2 d_in x r row-sharded: rows [i*d_in/N, ...)
       rc = src_ptr(A[0], (int64_t)d.d_in * rank, &sa);
@@ -883,15 +938,15 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
       e.offB[j] = curB;
       rc = gather_to(sb, dout, 0, i * w, rank / N, w, 0, p->arena + curB, st);
     } else if (d.parallel == BDLORA_COLUMN && d.sharding == BDLORA_SHARD_BD) {
-      // downward-compatible: compact (r/N_h) x d_out_j with N_h blocks side by side; the local
-      // B_1 [r/N, d_out_j/N] is block-diagonal with this device's m = N_h/N blocks
-      const int m = nb / N, rb = rank / nb, cb = dout / nb;
+      // downward-compatible: compact (r/N_h) x d_out_j with N_h blocks side by side; this device's
+      // m = N_h/N blocks (b = i*m + bb) are the columns [i*w, (i+1)*w) of it -- kept compact, [r/N_h, w]: the
+      // local B_1 [r/N, w] is block-diagonal and its zeros are never stored (the expand reads v rows
+      // [bb * r/N_h, (bb+1) * r/N_h) for the columns of block bb)
+      const int rb = rank / nb;
       rc = src_ptr(B[j], (int64_t)rb * dout, &sb);
       if (rc) break;
       e.offB[j] = curB;
-      if (cudaMemsetAsync(p->arena + curB, 0, (size_t)re * w * 2, st) != cudaSuccess) rc = fail(BDLORA_E_CUDA, "memset");
-      for (int bb = 0; bb < m && rc == BDLORA_OK; ++bb)
-        rc = gather_to(sb, dout, 0, (i * m + bb) * cb, rb, cb, 0, p->arena + curB + (int64_t)bb * rb * w + bb * cb, st, w);
+      rc = gather_to(sb, dout, 0, i * w, rb, w, 0, p->arena + curB, st);
     } else if (d.parallel == BDLORA_COLUMN) {
       // S-LoRA / NFS column: B_1 r x d_out_j column-sharded
       rc = src_ptr(B[j], (int64_t)rank * dout, &sb);
@@ -917,7 +972,7 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
       e.offB[0] = curB;
       rc = gather_to(sb, dout, 0, i * w, rank, w, 0, p->arena + curB, st);
     }
-    curB += (int64_t)re * w;
+    curB += (int64_t)(row ? re : re / m) * w;
   }
   if (rc != BDLORA_OK) {
     cudaStreamSynchronize(st);
@@ -933,6 +988,8 @@ static int load_adapter_impl(bdlora_pool* p, int32_t slot, int32_t rank, float s
     return rc;
   }
   retire_old();
+  if (row) p->g.ablk = m;
+  else p->g.bblk = m;
   p->h_tab[slot] = e;
   p->slot_elems[slot] = elems;
   p->resident_elems += elems;
@@ -1044,6 +1101,18 @@ int bdlora_base_expand(bdlora_pool* p, const void* X, int64_t T, const void* W, 
 static int bd_local(bdlora_pool* p, const void* X, int64_t T, const void* W, const int32_t* ids, void* Y, void* ws,
                     cudaStream_t st) {
   float* v = ws_v(p, ws, T);
+  if (pool_blocked(p)) {
+    // chunks of <= 64 tokens: shrink, then the decode kernel expanding that chunk's v (the next chunk's shrink
+    // overwrites v only after the expand completes: it waits on it, programmatic dependent launch)
+    for (int64_t c0 = 0; c0 < T; c0 += bdl::kDecMaxT) {
+      const int Tc = (int)std::min<int64_t>(T - c0, bdl::kDecMaxT);
+      const void* Xc = (const __nv_bfloat16*)X + (size_t)c0 * p->g.K;
+      float* vc = ws_v(p, ws, Tc);
+      ST_TRY(launch_shrink(p, Xc, Tc, ids + c0, vc, st, ws));
+      ST_TRY(launch_base_expand(p, Xc, Tc, W, ids + c0, vc, (__nv_bfloat16*)Y + (size_t)c0 * p->g.M, ws, st));
+    }
+    return BDLORA_OK;
+  }
   if (bdl::dec_enabled() && bdl::dec_eligible(p->g, (int)T) && decode_klocal_ok(p, (int)T)) {
     // decode: ONE lean kernel -- base GEMM on the tensor cores, K-local LoRA shrink + expand in its epilogue
     const int rc = launch_decode(p, X, (int)T, W, ids, nullptr, Y, ws, st, 1);

@@ -53,8 +53,11 @@ if slora:
 def fwd(i):
     W = Ws[i % nrep]
     if slora:
-        bd.bdlora_lora_shrink(pool, X, ids, vbuf, ws)
-        bd.bdlora_base_expand(pool, X, W, ids, vbuf, Y, ws)
+        only = os.environ.get("ONLY", "")  # shrink | expand: time one phase alone
+        if only != "expand":
+            bd.bdlora_lora_shrink(pool, X, ids, vbuf, ws)
+        if only != "shrink":
+            bd.bdlora_base_expand(pool, X, W, ids, vbuf, Y, ws)
     elif par == bd.COLUMN:
         bd.bdlora_column_forward(pool, X, W, ids, Y, ws)
     else:

@@ -359,6 +359,56 @@ def test_downward_compatible_integer_bit_exact(dev):
         assert np.array_equal(got, ref), f"row dev {i}: {np.count_nonzero(got != ref)} mismatches"
 
 
+@pytest.mark.parametrize("T", [64, 150])
+def test_downward_compatible_long_batches(dev, T):
+    """Downward-compatible serving beyond one 64-token decode batch (the library runs such pools in chunks of
+    <= 64 tokens): N_h = 8 adapters on N_l = 1 and 2, several adapters, id -1 tokens, vs the oracle."""
+    qkv, down = synth.arch_projections("llama-3.1-8b")[0], synth.arch_projections("llama-3.1-8b")[3]
+    for nl in (1, 2):
+        case = H.make_case(1800 + T + nl, qkv, "bd", 8, T, ranks=[16, 32, 8])
+        ref_full = ol.column_layer(case.X.f64, case.W.f64, qkv.d_out, case.oracle_adapters(), case.ids, "bd", 8)
+        _assert_tol(_np(_run_blocks(case, nl, nl - 1, dev)), ol.column_device_output(ref_full, nl, nl - 1),
+                    f"col 8->{nl} T={T}")
+        case = H.make_case(1900 + T + nl, down, "bd", 8, T, ranks=[16, 32])
+        P = _np(_run_blocks(case, nl, 0, dev))
+        _assert_tol(P, ol.row_partial_bd_blocks(case.X.f64, case.W.f64, case.oracle_adapters(), case.ids, 8, nl, 0),
+                    f"row 8->{nl} T={T}")
+
+
+def test_downward_compatible_stores_no_zeros(dev):
+    """P:389 / P:1082: the local blocks of a downward-compatible adapter are stored compactly -- resident bytes
+    are exactly those of the m = N_h / N_l diagonal blocks (COLUMN: B_j [r/N_h, d_out_j/N_l]; ROW: A
+    [r/N_l, d_in/N_h]), rounded up to whole K-rows; and one pool holds one block count."""
+    import paper_2510_23346_b200 as bd
+
+    qkv, down = synth.arch_projections("llama-3.1-8b")[0], synth.arch_projections("llama-3.1-8b")[3]
+    nh, r = 8, 32
+    for nl in (1, 2, 4):
+        for proj in (qkv, down):
+            case = H.make_case(2000 + nl, proj, "bd", nh, 1, ranks=[r])
+            par = bd.COLUMN if proj.parallel == "column" else bd.ROW
+            pool = bd.bdlora_create_pool(par, bd.SHARD_BD, nl, 0, proj.d_in, proj.d_out, 2, r)
+            ad = case.adapters[0]
+            bd.bdlora_load_adapter_blocks(pool, 0, r, ad.scale, [H.torch_bf16(x.bits) for x in ad.A],
+                                          [H.torch_bf16(x.bits) for x in ad.B], nh)
+            resident, _ = bd.bdlora_pool_bytes(pool)
+            K = proj.d_in if par == bd.COLUMN else proj.d_in // nl
+            if par == bd.COLUMN:
+                elems = sum((r // nl) * K + (r // nh) * (dj // nl) for dj in proj.d_out)
+                dense = sum((r // nl) * K + (r // nl) * (dj // nl) for dj in proj.d_out)
+            else:
+                elems = (r // nl) * (K // (nh // nl)) + (r // nl) * proj.d_out[0]
+                dense = (r // nl) * K + (r // nl) * proj.d_out[0]
+            assert resident == -(-elems // K) * K * 2, (nl, proj.name, resident, elems)
+            if nh // nl > 1:
+                assert resident < dense * 2
+                # a native (one-block) adapter cannot join a pool holding m > 1 blocks per device
+                with pytest.raises(bd.BdloraError):
+                    bd.bdlora_load_adapter(pool, 1, r, ad.scale, [H.torch_bf16(x.bits) for x in ad.A],
+                                           [H.torch_bf16(x.bits) for x in ad.B])
+            pool.close()
+
+
 # ----------------------------------------------------------------------------- Alg. 2 (P:1023-1046)
 
 def test_alg2_column_forward_gather(dev):

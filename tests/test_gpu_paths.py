@@ -219,8 +219,9 @@ def test_decode_chain_graph_replay(dev, T, pdl):
 
     bd.bdlora_set_pdl(pdl)
     try:
-        step()  # eager warm-up (also the first check below would catch eager errors)
+        step()  # eager run: the graph replay below must reproduce it bit for bit
         torch.cuda.synchronize()
+        eager = [[y.clone() for y in Yl] for Yl in Ys]
         for Yl in Ys:
             for y in Yl:
                 y.fill_(float("nan"))
@@ -238,7 +239,16 @@ def test_decode_chain_graph_replay(dev, T, pdl):
         bd.bdlora_set_pdl(True)
     for layer in range(L):
         for k in range(4):
-            _assert_tol(_np(Ys[k][layer]), ref[layer][k], f"layer {layer} proj {projs[k].name} T={T} pdl={pdl}")
+            what = f"layer {layer} proj {projs[k].name} T={T} pdl={pdl}"
+            # scheduling (graph replay, PDL) never changes a bit: every kernel reduces in a fixed order
+            assert torch.equal(Ys[k][layer].view(torch.int16), eager[k][layer].view(torch.int16)), what + " != eager"
+            # against the oracle chain: the GPU output of projection d (1-based depth in the chain) carries the
+            # rounding of the d - 1 projections before it; independent roundings add in quadrature, so the
+            # bound is sqrt(d) x the single-projection tolerance (reading R18)
+            d = 4 * layer + k + 1
+            ok, m, l1 = ol.within_tolerance(_np(Ys[k][layer]), ref[layer][k], max_rel=2e-2 * d ** 0.5,
+                                            l1_rel=5e-3 * d ** 0.5)
+            assert ok, f"{what}: max-rel {m:.3e} (<= {2e-2 * d ** 0.5:.2e}), l1-rel {l1:.3e} (<= {5e-3 * d ** 0.5:.2e})"
     for p in pools:
         p.close()
 
