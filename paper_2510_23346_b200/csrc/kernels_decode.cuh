@@ -525,6 +525,20 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
+    // Does the batch hold ONE adapter (plus id -1 tokens)?  The whole warp reads the <= 64 ids at once
+    // (a = the first non-negative id in token order, single = every non-negative id equals it): a serial
+    // scan by the elected thread would put up to 64 dependent L2 round trips before the first A box.
+    int w_a = -1;
+    bool w_single = true;
+    if (L::kTcShrink && LM == 1 && p.lora == 1 && p.tc_shrink) {
+      const int id0 = (lane < BN && lane < p.T) ? __ldg(p.ids + lane) : -1;
+      const int id1 = (lane + 32 < BN && lane + 32 < p.T) ? __ldg(p.ids + lane + 32) : -1;
+      const unsigned m0 = __ballot_sync(0xffffffffu, id0 >= 0), m1 = __ballot_sync(0xffffffffu, id1 >= 0);
+      const int s0 = __shfl_sync(0xffffffffu, id0, m0 ? __ffs(m0) - 1 : 0);
+      const int s1 = __shfl_sync(0xffffffffu, id1, m1 ? __ffs(m1) - 1 : 0);
+      w_a = m0 ? s0 : (m1 ? s1 : -1);
+      w_single = __all_sync(0xffffffffu, (id0 < 0 || id0 == w_a) && (id1 < 0 || id1 == w_a)) != 0;
+    }
     if (ptx::elect_one()) {
       const uint64_t pol_w = ptx::policy_evict_first();
       const uint64_t pol_x = ptx::policy_evict_last();
@@ -551,16 +565,8 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         return j == 0 ? arow_j[0] : j == 1 ? arow_j[1] : arow_j[2];
       };
       if (L::kTcShrink && LM == 1 && p.lora == 1 && p.tc_shrink && nu > 0) {
-        int a = -1;
-        bool single = true;
-#pragma unroll 16
-        for (int t = 0; t < BN; ++t) {
-          const int id = t < p.T ? __ldg(p.ids + t) : -1;
-          if (id >= 0) {
-            if (a < 0) a = id;
-            else if (id != a) single = false;
-          }
-        }
+        const int a = w_a;
+        const bool single = w_single;
         const int n0 = (u_lo / p.k_blocks) * kDecBM;
         const int jlo = dec_slice_of(p.g, n0), jhi = dec_slice_of(p.g, min(n0 + kDecBM, p.M) - 1);
         if (single && a >= 0 && jlo == jhi) {
