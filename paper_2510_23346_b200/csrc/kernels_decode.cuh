@@ -138,7 +138,10 @@ struct DecSmem {
   static constexpr int kVOpHalf = kMt ? 64 * kMtRows * 2 : 0;
   // cluster split-K: [s][ceil(128/s)][16] fp32 partial slots the peers push into (<= (128 + s) x 16 floats)
   static constexpr int kSlotOff = kVOpOff + 2 * kVOpHalf;
-  static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * BN * 4 : 0;
+  // a slot row is BN + 4 floats: consecutive rows start 16 bytes apart in the banks, so the contributors'
+  // float4 pushes (one row per thread) and the owner's float4 reads are bank-conflict free
+  static constexpr int kSlotStride = BN + 4;
+  static constexpr int kSlotBytes = CL ? (kDecBM + kDecMaxCluster) * kSlotStride * 4 : 0;
   static constexpr int kBytes = kSlotOff + kSlotBytes + 1024;   // + 1024-B alignment slack
   static constexpr int kVCol = 2 * BN;                          // TMEM: [acc 0 | acc 1 | v_seg 0 | v_seg 1]
   static constexpr int kTmemCols = BN == 16 ? (CL ? 64 : 32) : 256;
@@ -1259,7 +1262,7 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
           const int owner = ((row + 1) * sc_cl - 1) / kDecBM;
           const int rr = row - (owner * kDecBM) / sc_cl;
           const uint32_t dst =
-              ptx::mapa(ptx::smem_u32(s_slot + ((size_t)(crank * nr_max + rr) * BN + c0)), (uint32_t)owner);
+              ptx::mapa(ptx::smem_u32(s_slot + ((size_t)(crank * nr_max + rr) * L::kSlotStride + c0)), (uint32_t)owner);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (4 * q < tn)
@@ -1302,9 +1305,9 @@ __global__ void __launch_bounds__(kDecThreads, (S > 5 || BN > 16 ? 1 : 2))
         const int r_lo = (crank * kDecBM) / sc_cl, nr = ((crank + 1) * kDecBM) / sc_cl - r_lo;
         for (int f = etid; f < nr * nq; f += 128) {
           const int r2 = f % nr, qd = f / nr;
-          float4 y = *reinterpret_cast<const float4*>(s_slot + (size_t)r2 * BN + qd * 4);
+          float4 y = *reinterpret_cast<const float4*>(s_slot + (size_t)r2 * L::kSlotStride + qd * 4);
           for (int c = 1; c < sc_cl; ++c) {
-            const float4 z = *reinterpret_cast<const float4*>(s_slot + ((size_t)(c * nr_max + r2) * BN + qd * 4));
+            const float4 z = *reinterpret_cast<const float4*>(s_slot + ((size_t)(c * nr_max + r2) * L::kSlotStride + qd * 4));
             y.x += z.x, y.y += z.y, y.z += z.z, y.w += z.w;
           }
           const int nn = n0 + r_lo + r2;
