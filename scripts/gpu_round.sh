@@ -32,6 +32,8 @@ for w in $WHAT; do
         -o gpurun_out/prof_gateup_${TAG} -f python scripts/profile_one.py 28672 4096 1 16 fwd > /dev/null 2>&1
       timeout 300 ncu --set full --clock-control none --import-source on -k regex:dec_lora -s 3 -c 1 \
         -o gpurun_out/prof_mt_gateup_${TAG} -f python scripts/proj_profile.py llama-3.1-70b 2 8 64 8,16,32,64,128 128 uniform 4 > /dev/null 2>&1
+      ONLY=expand SHARDING=slora timeout 300 ncu --set full --clock-control none --import-source on -k regex:dec_lora -s 3 -c 1 \
+        -o gpurun_out/prof_slora_gateup_${TAG} -f python scripts/proj_profile.py llama-3.1-70b 2 8 64 8,16,32,64,128 128 uniform 4 > /dev/null 2>&1
       timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed \
         --clock-control none --csv --log-file gpurun_out/launches_prefill_${TAG}.csv \
         python scripts/proj_profile.py llama-3.1-8b 2 8 1024 64 1 single 3 > /dev/null 2>&1
