@@ -1,7 +1,8 @@
 """Multi-process host logic of the N > 1 path on CPU (gloo, world size 2, 127.0.0.1):
 the NCCL unique-id bootstrap over torch.distributed, the bench's max-over-ranks timing reduction,
-and Alg. 1's row-layer all-reduce emulated with gloo over the oracle's per-rank partials
-(sum of device partials == unsharded layer)."""
+Alg. 1's row-layer all-reduce emulated with gloo over the oracle's per-rank partials
+(sum of device partials == unsharded layer), and Alg. 2's all-gather of the column blocks
+(rank-order concatenation == unsharded column output)."""
 import os
 import socket
 
@@ -55,7 +56,26 @@ def _worker(rank, world, port, q):
         dist.all_reduce(P)
         full = ol.row_layer(X, W, ads, ids, "bd", world)
         err = float(np.max(np.abs(P.numpy() - full)))
-        q.put((rank, uid, ids_all, mx, err))
+        # 4) Alg. 2: every rank's column block, all-gathered in rank order, is the unsharded
+        #    column output [Y_0 | Y_1] (n_slices = 1) -- for one token (the in-place gather of
+        #    bdlora_column_forward_gather) and for several
+        col = synth.tiny_pair()[0]
+        cads = {}
+        for a in range(3):
+            ad = synth.make_adapter(rng, col, "bd", 8, world, 2.0)
+            cads[a] = {"rank": 8, "scale": ad.scale, "A": [x.f64 for x in ad.A], "B": [x.f64 for x in ad.B]}
+        Wc = synth.make_base(rng, col).f64
+        gerr = 0.0
+        for T in (1, 9):
+            Xc = synth.make_x(rng, T, col.d_in).f64
+            cid = ids[:T]
+            yfull = ol.column_layer(Xc, Wc, col.d_out, cads, cid, "bd", world)
+            mine = torch.from_numpy(np.ascontiguousarray(ol.column_device_output(yfull, world, rank)))
+            parts = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(parts, mine)
+            gathered = torch.cat(parts, dim=1).numpy()
+            gerr = max(gerr, float(np.max(np.abs(gathered - np.concatenate(yfull, axis=1)))))
+        q.put((rank, uid, ids_all, mx, max(err, gerr)))
     finally:
         dist.destroy_process_group()
 
