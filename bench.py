@@ -642,7 +642,10 @@ def run_ours(args, wl):
         except Exception:
             traffic = None
     roofline = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-                "traffic": traffic, "kernel": f"{dom} projection (shrink + base GEMV/GEMM with fused expand)",
+                "traffic": traffic,
+                "traffic_source": ("ncu --set full capture of this kernel and shape, profiles/traffic.json "
+                                   "(not measured in this run)") if traffic is not None else None,
+                "kernel": f"{dom} projection (shrink + base GEMV/GEMM with fused expand)",
                 "algorithmic_bytes": dom_bytes, "algorithmic_flops": dom_flops, "mean_us": dom_mean_us,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)" if bound == "hbm" else peak_src}
     layer_bytes = sum(b for b, _ in alg.values())

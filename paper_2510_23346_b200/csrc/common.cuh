@@ -3,16 +3,53 @@
 // Pool layout in HBM: one bf16 arena per pool; each loaded slot keeps
 // only this device's shard of its factors, stored compactly (no zero of a block-diagonal factor is
 // stored):
-//   A_j : [rs, K]   rank-outermost, K contiguous  (the shrink streams whole 128-bit rows)
+//   A_j : [rs, K]   rank-outermost, K contiguous  (the shrink streams whole 128-bit rows; a downward-
+//         compatible ROW adapter keeps only its rows' own block: [rs, K/m])
 //   B_j : [re, ldb_j] row-major, output columns contiguous (the expand epilogue reads a row of B
 //         across consecutive output columns -> coalesced)
 // and one 64-byte SlotEntry in a device table indexed by the adapter id.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace bdl {
+
+// Host: memo of the TMA tensor maps a forward encodes for its W and X ([rows, K] bf16, K-major, boxes of
+// 64 x box_rows, 128B swizzle -- the only maps the launchers build per call).  The 128-byte map is a pure
+// function of (base, K, rows, box_rows), so an eager caller that reuses its buffers skips
+// cuTensorMapEncodeTiled (a CUDA graph bakes the maps in at capture anyway).  Per host thread, 64 entries,
+// round-robin replacement.
+struct TmapMemo {
+  static constexpr int kN = 64;
+  const void* base[kN];
+  int K[kN], rows[kN], box[kN];
+  CUtensorMap map[kN];
+  int n = 0, next = 0;
+};
+inline TmapMemo& tmap_memo() {
+  static thread_local TmapMemo m;
+  return m;
+}
+inline bool tmap_memo_get(const void* base, int K, int rows, int box, CUtensorMap* out) {
+  TmapMemo& m = tmap_memo();
+  for (int i = 0; i < m.n; ++i)
+    if (m.base[i] == base && m.K[i] == K && m.rows[i] == rows && m.box[i] == box) {
+      *out = m.map[i];
+      return true;
+    }
+  return false;
+}
+inline void tmap_memo_put(const void* base, int K, int rows, int box, const CUtensorMap& map) {
+  TmapMemo& m = tmap_memo();
+  const int i = m.n < TmapMemo::kN ? m.n++ : (m.next++ % TmapMemo::kN);
+  m.base[i] = base;
+  m.K[i] = K;
+  m.rows[i] = rows;
+  m.box[i] = box;
+  m.map[i] = map;
+}
 
 constexpr int kMaxSlices = 3;
 

@@ -1278,6 +1278,7 @@ inline PFN_encodeTiled get_encode_fn() {
 
 // 2D bf16 K-major tensor [rows, K] with box [box_rows, 64], SWIZZLE_128B, OOB -> zeros.
 inline bool encode_kmajor(CUtensorMap* m, const void* base, int K, int rows, int box_rows) {
+  if (tmap_memo_get(base, K, rows, box_rows, m)) return true;
   PFN_encodeTiled enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
@@ -1287,7 +1288,9 @@ inline bool encode_kmajor(CUtensorMap* m, const void* base, int K, int rows, int
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  tmap_memo_put(base, K, rows, box_rows, *m);
+  return true;
 }
 
 // Ring depth.  Measured (scripts/stages_sweep.sh, 8B decode layer): 2 stages 134 us, 3: 103, 4: 100,
